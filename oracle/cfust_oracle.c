@@ -1,0 +1,736 @@
+/*
+ * ORACLE — TEST INFRASTRUCTURE ONLY (see cfust_oracle.h).
+ *
+ * Plain FP64 CPU implementation of one FM-CFUST EM iteration, written from the paper
+ * (arXiv 2005.06848, /root/reference/PAPER.md) and the readings in DESIGN.md §3 where the
+ * paper omits the CFUST E-/M-step ("technical details ... omitted", PAPER.md:194-195;
+ * "eight partial sums ... equations (27) to (34) in [llm19]").
+ *
+ * Notation: r = y - mu, d = r' Omega^{-1} r, c = Delta' Omega^{-1} r,
+ * m0 = nu + p, rho = nu + d, S' = (rho/m0) Lambda.  T_r(b; 0, S, m) = P(X <= b),
+ * X ~ t_r(0, S, m).  No blocking, fusion or reordering beyond the formulas; per-pair work
+ * may run on several threads (independent pairs), the sums are accumulated serially in
+ * ascending j.
+ *
+ * Build: gcc -O2 -ffp-contract=off -fopenmp -shared -fPIC cfust_oracle.c -lm
+ */
+#include "cfust_oracle.h"
+
+#include <math.h>
+#include <stdlib.h>
+#include <string.h>
+#ifdef _OPENMP
+#include <omp.h>
+#endif
+
+#define QMAX 8
+#define PMAX 8
+static const double ORC_PI = 3.14159265358979323846;
+static const double ORC_UMIN = 1e-300;                 /* reading A15 */
+static const double ORC_UMAX = 0x1.fffffffffffffp-1;   /* largest double < 1, reading A15 */
+
+/* =====================================================================================
+ * Special functions (pins C12: tests/test_oracle_special.py against scipy / mpmath)
+ * ===================================================================================== */
+
+/* Standard normal CDF via the C library erfc: Phi(x) = erfc(-x/sqrt 2)/2. */
+double orc_norm_cdf(double x) { return 0.5 * erfc(-x / sqrt(2.0)); }
+
+static double norm_pdf(double x) { return exp(-0.5 * x * x) / sqrt(2.0 * ORC_PI); }
+
+/* Phi^{-1}(u): the root of log Phi(z) = log u, by bisection-safeguarded Newton started from
+ * the Abramowitz & Stegun 26.2.23 approximation.  u > 1/2 uses symmetry with 1-u (exact). */
+double orc_norm_quantile(double u) {
+    if (!(u > 0.0)) return -INFINITY;
+    if (!(u < 1.0)) return INFINITY;
+    if (u == 0.5) return 0.0;
+    if (u > 0.5) return -orc_norm_quantile(1.0 - u);
+    const double lu = log(u);
+    const double t = sqrt(-2.0 * lu);
+    double z = -(t - (2.515517 + 0.802853 * t + 0.010328 * t * t) /
+                         (1.0 + 1.432788 * t + 0.189269 * t * t + 0.001308 * t * t * t));
+    double lo = -40.0, hi = 0.0;
+    for (int it = 0; it < 200; ++it) {
+        const double P = orc_norm_cdf(z);
+        const double h = log(P) - lu;                 /* increasing in z */
+        if (h == 0.0) return z;
+        if (h > 0.0) hi = z; else lo = z;
+        double zn = z - h * P / norm_pdf(z);          /* Newton on log Phi */
+        if (fabs(zn - z) <= 1e-12 * fmax(1.0, fabs(z))) return zn;  /* quadratic: error ~ step^2 */
+        if (!(zn > lo && zn < hi)) zn = 0.5 * (lo + hi);
+        z = zn;
+    }
+    return z;
+}
+
+/* Regularized incomplete gamma P(a,x): power series, valid for x < a+1. */
+static double gamma_p_series(double a, double x) {
+    double term = 1.0 / a, sum = term;
+    for (int n = 1; n < 100000; ++n) {
+        term *= x / (a + n);
+        sum += term;
+        if (fabs(term) < fabs(sum) * 1e-17) break;
+    }
+    return sum * exp(-x + a * log(x) - lgamma(a));
+}
+
+/* Regularized incomplete gamma Q(a,x): Legendre continued fraction (modified Lentz), x >= a+1. */
+static double gamma_q_cf(double a, double x) {
+    const double tiny = 1e-300;
+    double b = x + 1.0 - a, c = 1.0 / tiny, d = 1.0 / b, h = d;
+    for (int i = 1; i < 100000; ++i) {
+        const double an = -i * (i - a);
+        b += 2.0;
+        d = an * d + b; if (fabs(d) < tiny) d = tiny;
+        c = b + an / c; if (fabs(c) < tiny) c = tiny;
+        d = 1.0 / d;
+        const double del = d * c;
+        h *= del;
+        if (fabs(del - 1.0) < 1e-16) break;
+    }
+    return exp(-x + a * log(x) - lgamma(a)) * h;
+}
+
+double orc_gamma_p(double a, double x) {
+    if (!(x > 0.0)) return 0.0;
+    if (isinf(x)) return 1.0;
+    return (x < a + 1.0) ? gamma_p_series(a, x) : 1.0 - gamma_q_cf(a, x);
+}
+
+double orc_gamma_q(double a, double x) {
+    if (!(x > 0.0)) return 1.0;
+    if (isinf(x)) return 0.0;
+    return (x < a + 1.0) ? 1.0 - gamma_p_series(a, x) : gamma_q_cf(a, x);
+}
+
+/* Chi-square quantile with real df m: v such that P(m/2, v/2) = w.  For w > 1/2 the
+ * equivalent equation Q(m/2, v/2) = 1-w (1-w exact) is solved.  Newton in t = log(v/2) on
+ * log F, safeguarded by bisection in t.  Started from the Wilson-Hilferty approximation. */
+double orc_chi2_quantile(double w, double m) {
+    if (!(w > 0.0)) return 0.0;
+    if (!(w < 1.0)) return INFINITY;
+    const double a = 0.5 * m;
+    const int upper = w > 0.5;
+    const double lt = log(upper ? 1.0 - w : w);
+    /* initial guess */
+    const double zq = orc_norm_quantile(w);
+    const double k9 = 2.0 / (9.0 * m);
+    double v0 = m * pow(1.0 - k9 + zq * sqrt(k9), 3.0);
+    if (!(v0 > 0.0)) v0 = 2.0 * exp((log(w) + lgamma(a + 1.0)) / a);   /* P ~ x^a / Gamma(a+1) */
+    double t = log(0.5 * v0);
+    double tlo = -745.0, thi = log(fmax(1.0, a)) ;
+    /* expand upper bracket until F(e^thi) is past the target */
+    for (int it = 0; it < 200; ++it) {
+        const double x = exp(thi);
+        const double F = upper ? orc_gamma_q(a, x) : orc_gamma_p(a, x);
+        const double h = log(F) - lt;
+        if (upper ? (h < 0.0) : (h > 0.0)) break;
+        thi += 1.0;
+    }
+    if (!(t > tlo && t < thi)) t = 0.5 * (tlo + thi);
+    for (int it = 0; it < 400; ++it) {
+        const double x = exp(t);
+        const double F = upper ? orc_gamma_q(a, x) : orc_gamma_p(a, x);
+        const double h = log(F) - lt;   /* increasing in t for P, decreasing for Q */
+        if (h == 0.0) break;
+        if ((h > 0.0) != upper) thi = t; else tlo = t;
+        /* d log F / dt = x * pdf(x) / F (sign - for Q) */
+        const double lpdf = (a - 1.0) * log(x) - x - lgamma(a);
+        double dh = exp(log(x) + lpdf) / F;
+        if (upper) dh = -dh;
+        double tn = t - h / dh;
+        if (fabs(tn - t) <= 1e-12 * fmax(1.0, fabs(t))) { t = tn; break; }  /* quadratic */
+        if (!(tn > tlo && tn < thi)) tn = 0.5 * (tlo + thi);
+        t = tn;
+    }
+    return 2.0 * exp(t);
+}
+
+/* Continued fraction for the incomplete beta function (modified Lentz). */
+static double betacf(double a, double b, double x) {
+    const double tiny = 1e-300;
+    const double qab = a + b, qap = a + 1.0, qam = a - 1.0;
+    double c = 1.0, d = 1.0 - qab * x / qap;
+    if (fabs(d) < tiny) d = tiny;
+    d = 1.0 / d;
+    double h = d;
+    for (int k = 1; k < 100000; ++k) {
+        const double k2 = 2.0 * k;
+        double aa = k * (b - k) * x / ((qam + k2) * (a + k2));
+        d = 1.0 + aa * d; if (fabs(d) < tiny) d = tiny;
+        c = 1.0 + aa / c; if (fabs(c) < tiny) c = tiny;
+        d = 1.0 / d;
+        h *= d * c;
+        aa = -(a + k) * (qab + k) * x / ((a + k2) * (qap + k2));
+        d = 1.0 + aa * d; if (fabs(d) < tiny) d = tiny;
+        c = 1.0 + aa / c; if (fabs(c) < tiny) c = tiny;
+        d = 1.0 / d;
+        const double del = d * c;
+        h *= del;
+        if (fabs(del - 1.0) < 1e-16) break;
+    }
+    return h;
+}
+
+/* Regularized incomplete beta I_x(a,b); xc = 1-x supplied separately for accuracy. */
+double orc_ibeta(double a, double b, double x, double xc) {
+    if (!(x > 0.0)) return 0.0;
+    if (!(xc > 0.0)) return 1.0;
+    const double lx = (x < 0.5) ? log(x) : log1p(-xc);
+    const double lxc = (xc < 0.5) ? log(xc) : log1p(-x);
+    const double lfront = a * lx + b * lxc - (lgamma(a) + lgamma(b) - lgamma(a + b));
+    if (x < (a + 1.0) / (a + b + 2.0)) return exp(lfront) * betacf(a, b, x) / a;
+    return 1.0 - exp(lfront) * betacf(b, a, xc) / b;
+}
+
+/* Univariate Student-t CDF with real df m: T_m(x) = 1 - I_{m/(m+x^2)}(m/2, 1/2)/2 for x >= 0. */
+double orc_t_cdf(double x, double m) {
+    if (isnan(x)) return NAN;
+    if (isinf(x)) return x > 0 ? 1.0 : 0.0;
+    const double x2 = x * x;
+    const double tail = 0.5 * orc_ibeta(0.5 * m, 0.5, m / (m + x2), x2 / (m + x2));
+    return x >= 0.0 ? 1.0 - tail : tail;
+}
+
+/* log t_1(x; loc, s2, m): univariate t density with location loc, scale^2 s2, df m. */
+double orc_t1_logpdf(double x, double loc, double s2, double m) {
+    const double u = (x - loc) * (x - loc) / (m * s2);
+    return lgamma(0.5 * (m + 1.0)) - lgamma(0.5 * m) - 0.5 * log(m * ORC_PI * s2)
+           - 0.5 * (m + 1.0) * log1p(u);
+}
+
+/* Digamma: recurrence psi(x) = psi(x+1) - 1/x up to x >= 10, then the asymptotic series. */
+double orc_digamma(double x) {
+    double r = 0.0;
+    while (x < 10.0) { r -= 1.0 / x; x += 1.0; }
+    const double f = 1.0 / (x * x);
+    const double t = f * (-1.0 / 12 + f * (1.0 / 120 + f * (-1.0 / 252 + f * (1.0 / 240 +
+                     f * (-1.0 / 132 + f * (691.0 / 32760 + f * (-1.0 / 12)))))));
+    return r + log(x) - 0.5 / x + t;
+}
+
+/* =====================================================================================
+ * Small dense linear algebra (row-major)
+ * ===================================================================================== */
+static int chol(int n, const double *S, double *L) {
+    memset(L, 0, sizeof(double) * n * n);
+    for (int i = 0; i < n; ++i)
+        for (int j = 0; j <= i; ++j) {
+            double s = S[i * n + j];
+            for (int k = 0; k < j; ++k) s -= L[i * n + k] * L[j * n + k];
+            if (i == j) {
+                if (!(s > 1e-300)) return ORC_ENOTPD;   /* SPEC.md:125 pivot rule */
+                L[i * n + i] = sqrt(s);
+            } else {
+                L[i * n + j] = s / L[j * n + j];
+            }
+        }
+    return ORC_OK;
+}
+
+/* solve L L' x = b in place */
+static void chol_solve(int n, const double *L, double *x) {
+    for (int i = 0; i < n; ++i) {
+        double s = x[i];
+        for (int k = 0; k < i; ++k) s -= L[i * n + k] * x[k];
+        x[i] = s / L[i * n + i];
+    }
+    for (int i = n - 1; i >= 0; --i) {
+        double s = x[i];
+        for (int k = i + 1; k < n; ++k) s -= L[k * n + i] * x[k];
+        x[i] = s / L[i * n + i];
+    }
+}
+
+int orc_k_stats(int p, int q) { return 3 + p + p * (p + 1) / 2 + q + q * (q + 1) / 2 + p * q; }
+
+/* =====================================================================================
+ * Lattice (O0; readings A11, A12): x = frac((l z_k mod M)/M + shift_k), w = |2x - 1|.
+ * ===================================================================================== */
+double orc_lattice_w(const orc_lattice *L, int64_t l, int k) {
+    const uint64_t t = ((uint64_t)l * (uint64_t)L->z[k]) % (uint64_t)L->M;
+    double x = (double)t / (double)L->M + L->shift[k];
+    if (x >= 1.0) x -= 1.0;
+    return fabs(2.0 * x - 1.0);
+}
+
+/* Chi radius nodes for df m: s_l = sqrt(chi2_m^{-1}(w_{l,0}) / m)  (reading R-T). */
+void orc_chi_table(const orc_lattice *L, double m, double *s_out) {
+    for (int64_t l = 0; l < L->M; ++l) s_out[l] = sqrt(orc_chi2_quantile(orc_lattice_w(L, l, 0), m) / m);
+}
+
+/* =====================================================================================
+ * T_r(b; 0, S, m) — Genz-Bretz separation of variables for the multivariate t in its
+ * chi-normal form (reading R-T):  T_r(b;S,m) = E_V[ Phi_r( b sqrt(V/m); S ) ],
+ * V ~ chi^2_m.  Lattice coordinate 0 gives V, coordinates 1..r-1 the normal SOV steps.
+ * Variables are reordered by ascending b_k/sqrt(S_kk), stable (reading A13/A14).
+ * r = 0 -> 1;  r = 1 -> closed form T_m(b/sqrt(S)).
+ * ===================================================================================== */
+double orc_Tr(int r, const double *b, const double *S, double m, const orc_lattice *L,
+              const double *chi_s, double *min_key_gap) {
+    if (r == 0) return 1.0;
+    if (r == 1) return orc_t_cdf(b[0] / sqrt(S[0]), m);
+    int perm[QMAX];
+    double key[QMAX];
+    for (int k = 0; k < r; ++k) { perm[k] = k; key[k] = b[k] / sqrt(S[k * r + k]); }
+    for (int i = 1; i < r; ++i) {   /* stable insertion sort by key */
+        const int pi = perm[i];
+        int j = i - 1;
+        while (j >= 0 && key[perm[j]] > key[pi]) { perm[j + 1] = perm[j]; --j; }
+        perm[j + 1] = pi;
+    }
+    if (min_key_gap) {
+        for (int i = 1; i < r; ++i) {
+            const double a = key[perm[i - 1]], bb = key[perm[i]];
+            const double gap = fabs(bb - a) / fmax(1.0, fmax(fabs(a), fabs(bb)));
+            if (gap < *min_key_gap) *min_key_gap = gap;
+        }
+    }
+    double Sp[QMAX * QMAX], bp[QMAX], C[QMAX * QMAX];
+    for (int i = 0; i < r; ++i) {
+        bp[i] = b[perm[i]];
+        for (int j = 0; j < r; ++j) Sp[i * r + j] = S[perm[i] * r + perm[j]];
+    }
+    if (chol(r, Sp, C) != ORC_OK) return NAN;
+    double sum = 0.0;
+    for (int64_t l = 0; l < L->M; ++l) {
+        const double s = chi_s[l];
+        double e = orc_norm_cdf(s * bp[0] / C[0]);
+        double f = e;
+        double zz[QMAX];
+        for (int k = 1; k < r; ++k) {
+            double u = orc_lattice_w(L, l, k) * e;
+            if (u < ORC_UMIN) u = ORC_UMIN;
+            if (u > ORC_UMAX) u = ORC_UMAX;
+            zz[k - 1] = orc_norm_quantile(u);
+            double acc = s * bp[k];
+            for (int t = 0; t < k; ++t) acc -= C[k * r + t] * zz[t];
+            e = orc_norm_cdf(acc / C[k * r + k]);
+            f *= e;
+        }
+        sum += f;
+    }
+    return sum / (double)L->M;
+}
+
+/* =====================================================================================
+ * O1: per-component derived quantities (Eq. (2) definitions)
+ *   Omega = Sigma + Delta Delta', L_omega = chol(Omega), A = Delta' Omega^{-1} (q x p),
+ *   Lambda = I_q - Delta' Omega^{-1} Delta (symmetrised),
+ *   kappa = lgamma((nu+p)/2) - lgamma(nu/2) - (p/2) log(nu pi) - (1/2) log|Omega|.
+ * ===================================================================================== */
+int orc_derive(int p, int q, const double *sigma, const double *delta, double nu,
+               double *L_omega, double *A, double *Lambda, double *logdet, double *kappa) {
+    double Om[PMAX * PMAX];
+    for (int a = 0; a < p; ++a)
+        for (int b = 0; b < p; ++b) {
+            double s = sigma[a * p + b];
+            for (int k = 0; k < q; ++k) s += delta[a * q + k] * delta[b * q + k];
+            Om[a * p + b] = s;
+        }
+    if (chol(p, Om, L_omega) != ORC_OK) return ORC_ENOTPD;
+    double ld = 0.0;
+    for (int a = 0; a < p; ++a) ld += 2.0 * log(L_omega[a * p + a]);
+    *logdet = ld;
+    for (int k = 0; k < q; ++k) {          /* column k of Omega^{-1} Delta */
+        double x[PMAX];
+        for (int a = 0; a < p; ++a) x[a] = delta[a * q + k];
+        chol_solve(p, L_omega, x);
+        for (int a = 0; a < p; ++a) A[k * p + a] = x[a];
+    }
+    for (int k = 0; k < q; ++k)
+        for (int l = 0; l < q; ++l) {
+            double s = 0.0;
+            for (int a = 0; a < p; ++a) s += delta[a * q + k] * A[l * p + a];
+            Lambda[k * q + l] = (k == l ? 1.0 : 0.0) - s;
+        }
+    for (int k = 0; k < q; ++k)
+        for (int l = k + 1; l < q; ++l) {
+            const double s = 0.5 * (Lambda[k * q + l] + Lambda[l * q + k]);
+            Lambda[k * q + l] = Lambda[l * q + k] = s;
+        }
+    const double m0 = nu + p;
+    *kappa = lgamma(0.5 * m0) - lgamma(0.5 * nu) - 0.5 * p * log(nu * ORC_PI) - 0.5 * ld;
+    return ORC_OK;
+}
+
+/* =====================================================================================
+ * O2-O8: one (observation, component) pair.
+ * out = [log(2^q t_p T0)  (no log pi),  e1-e2,  e2,  e3 (q),  e4 (q*q)]
+ * ===================================================================================== */
+int orc_pair(int p, int q, const double *y, const double *mu, const double *L_omega,
+             const double *A, const double *Lambda, double nu, double kappa,
+             const orc_lattice *L, const double *chi_m0, const double *chi_m1,
+             const double *chi_m2, double *out, double *min_key_gap) {
+    double r[PMAX], v[PMAX];
+    for (int a = 0; a < p; ++a) r[a] = y[a] - mu[a];
+    for (int a = 0; a < p; ++a) {          /* forward solve L v = r; d = |v|^2 */
+        double s = r[a];
+        for (int b = 0; b < a; ++b) s -= L_omega[a * p + b] * v[b];
+        v[a] = s / L_omega[a * p + a];
+    }
+    double d = 0.0;
+    for (int a = 0; a < p; ++a) d += v[a] * v[a];
+    const double m0 = nu + p, rho = nu + d;
+    const double logt = kappa - 0.5 * m0 * log1p(d / nu);              /* log t_p(y; mu, Omega, nu) */
+    const double e1me2 = orc_digamma(0.5 * m0) - log(0.5 * rho) - m0 / rho;   /* reading A5 (R1) */
+    out[1] = e1me2;
+    if (q == 0) {                            /* Delta = 0: t-mixture */
+        out[0] = logt;
+        out[2] = m0 / rho;
+        return ORC_OK;
+    }
+    double c[QMAX];
+    for (int k = 0; k < q; ++k) {
+        double s = 0.0;
+        for (int a = 0; a < p; ++a) s += A[k * p + a] * r[a];
+        c[k] = s;
+    }
+    /* T0 for the density (Eq. (2)), T2 for e2 */
+    double bq[QMAX];
+    for (int k = 0; k < q; ++k) bq[k] = c[k] * sqrt(m0 / rho);
+    const double T0 = orc_Tr(q, bq, Lambda, m0, L, chi_m0, min_key_gap);
+    for (int k = 0; k < q; ++k) bq[k] = c[k] * sqrt((m0 + 2.0) / rho);
+    const double T2 = orc_Tr(q, bq, Lambda, m0 + 2.0, L, chi_m2, min_key_gap);
+    const int PW = 3 + q + q * q;
+    if (!(T0 > 0.0)) {                       /* reading A16: f_ij = 0 */
+        out[0] = -INFINITY;
+        for (int k = 2; k < PW; ++k) out[k] = 0.0;
+        return ORC_OK;
+    }
+    double Sp[QMAX * QMAX];                  /* S' = (rho/m0) Lambda */
+    for (int k = 0; k < q * q; ++k) Sp[k] = (rho / m0) * Lambda[k];
+
+    /* O6: h_k = t_1(0; c_k, S'_kk, m0) * T_{q-1}(c~(k); 0, S~(k), m0+1) */
+    const int q1 = q - 1;
+    double phi[QMAX], Tk[QMAX], h[QMAX];
+    double ct[QMAX][QMAX], St[QMAX][QMAX * QMAX], Stp[QMAX][QMAX * QMAX];
+    int oth[QMAX][QMAX];
+    for (int k = 0; k < q; ++k) {
+        phi[k] = exp(orc_t1_logpdf(0.0, c[k], Sp[k * q + k], m0));
+        Tk[k] = 1.0;
+        if (q >= 2) {
+            int na = 0;
+            for (int t = 0; t < q; ++t) if (t != k) oth[k][na++] = t;
+            const double skk = Sp[k * q + k];
+            const double fac = (m0 + c[k] * c[k] / skk) / (m0 + 1.0);
+            for (int a = 0; a < q1; ++a) {
+                const int ia = oth[k][a];
+                ct[k][a] = c[ia] - Sp[ia * q + k] * c[k] / skk;
+                for (int b = 0; b < q1; ++b) {
+                    const int ib = oth[k][b];
+                    St[k][a * q1 + b] = fac * (Sp[ia * q + ib] - Sp[ia * q + k] * Sp[k * q + ib] / skk);
+                }
+            }
+            Tk[k] = orc_Tr(q1, ct[k], St[k], m0 + 1.0, L, chi_m1, min_key_gap);
+            for (int a = 0; a < q1 * q1; ++a) Stp[k][a] = ((m0 + 1.0) / (m0 - 1.0)) * St[k][a];
+        }
+        h[k] = phi[k] * Tk[k];
+    }
+    /* O7: E1 = E[X 1{X>0}], X ~ t_q(c, S, m0+2):  E1 = c T2 + S' h */
+    double E1[QMAX];
+    for (int a = 0; a < q; ++a) {
+        double s = c[a] * T2;
+        for (int k = 0; k < q; ++k) s += Sp[a * q + k] * h[k];
+        E1[a] = s;
+    }
+    /* G_kl = phi_k * E[X_l 1{X_-k > 0} | X_k = 0] (first moment of the conditional truncated t):
+     *      = phi_k [ c~(k)_l T~(k) + (S~'(k) h(k))_l ],  G_kk = 0,
+     * h(k)_t = t_1(0; c~(k)_t, S~'(k)_tt, m0-1) * T_{q-2}(c^(k,t); 0, S^(k,t), m0). */
+    double G[QMAX * QMAX];
+    memset(G, 0, sizeof(G));
+    if (q >= 2) {
+        const int q2 = q - 2;
+        double Tkt[QMAX][QMAX];
+        for (int k = 0; k < q; ++k)
+            for (int t = k + 1; t < q; ++t) {
+                double val = 1.0;
+                if (q2 >= 1) {
+                    int at = -1;
+                    for (int a = 0; a < q1; ++a) if (oth[k][a] == t) at = a;
+                    const double saa = Stp[k][at * q1 + at];
+                    const double fac2 = (m0 - 1.0 + ct[k][at] * ct[k][at] / saa) / m0;
+                    double ch[QMAX], Sh[QMAX * QMAX];
+                    int rest[QMAX], nr = 0;
+                    for (int a = 0; a < q1; ++a) if (a != at) rest[nr++] = a;
+                    for (int a = 0; a < q2; ++a) {
+                        const int ra = rest[a];
+                        ch[a] = ct[k][ra] - Stp[k][ra * q1 + at] * ct[k][at] / saa;
+                        for (int b = 0; b < q2; ++b) {
+                            const int rb = rest[b];
+                            Sh[a * q2 + b] = fac2 * (Stp[k][ra * q1 + rb] -
+                                                     Stp[k][ra * q1 + at] * Stp[k][at * q1 + rb] / saa);
+                        }
+                    }
+                    val = orc_Tr(q2, ch, Sh, m0, L, chi_m0, min_key_gap);
+                }
+                Tkt[k][t] = Tkt[t][k] = val;   /* symmetric in {k,t}: evaluated once (A17) */
+            }
+        for (int k = 0; k < q; ++k) {
+            double hk[QMAX];
+            for (int a = 0; a < q1; ++a) {
+                const int t = oth[k][a];
+                hk[a] = exp(orc_t1_logpdf(0.0, ct[k][a], Stp[k][a * q1 + a], m0 - 1.0)) * Tkt[k][t];
+            }
+            for (int a = 0; a < q1; ++a) {
+                double s = ct[k][a] * Tk[k];
+                for (int b = 0; b < q1; ++b) s += Stp[k][a * q1 + b] * hk[b];
+                G[k * q + oth[k][a]] = phi[k] * s;
+            }
+        }
+    }
+    /* E2 = E[X X' 1{X>0}] = sym( S'(G + T0 I) + c E1' ) */
+    double E2[QMAX * QMAX];
+    for (int a = 0; a < q; ++a)
+        for (int b = 0; b < q; ++b) {
+            double s = 0.0;
+            for (int k = 0; k < q; ++k) s += Sp[a * q + k] * (G[k * q + b] + (k == b ? T0 : 0.0));
+            E2[a * q + b] = s + c[a] * E1[b];
+        }
+    /* O8 */
+    const double fac = m0 / rho;
+    out[0] = q * log(2.0) + logt + log(T0);
+    out[2] = fac * T2 / T0;
+    for (int a = 0; a < q; ++a) out[3 + a] = fac * E1[a] / T0;
+    for (int a = 0; a < q; ++a)
+        for (int b = 0; b < q; ++b)
+            out[3 + q + a * q + b] = fac * 0.5 * (E2[a * q + b] + E2[b * q + a]) / T0;
+    return ORC_OK;
+}
+
+/* =====================================================================================
+ * E-step over all observations: Eq. (3)-(4), Alg. 2
+ * with the sums S0..S7 (reading A4) accumulated in ascending j.
+ * ===================================================================================== */
+typedef struct {
+    double L[PMAX * PMAX], A[QMAX * PMAX], Lam[QMAX * QMAX], logdet, kappa;
+    double *chi0, *chi1, *chi2;
+} comp_derived;
+
+int orc_estep(int64_t n, int p, int q, int g, const double *y,
+              const double *pi, const double *mu, const double *sigma,
+              const double *delta, const double *nu, const orc_lattice *L,
+              int nthreads, double *pair_out, double *stats, double *loglik,
+              double *min_key_gap) {
+    if (p < 1 || p > PMAX || q < 0 || q > 6 || g < 1 || n < 0) return ORC_EINVAL;
+    const int need_lattice = q >= 2;
+    if (need_lattice && (L == NULL || L->s < q)) return ORC_EINVAL;
+    comp_derived *cd = (comp_derived *)calloc(g, sizeof(comp_derived));
+    int rc = ORC_OK;
+    for (int i = 0; i < g && rc == ORC_OK; ++i) {
+        rc = orc_derive(p, q, sigma + (size_t)i * p * p, delta + (size_t)i * p * q, nu[i],
+                        cd[i].L, cd[i].A, cd[i].Lam, &cd[i].logdet, &cd[i].kappa);
+        if (rc == ORC_OK && need_lattice) {
+            const double m0 = nu[i] + p;
+            cd[i].chi0 = (double *)malloc(sizeof(double) * L->M);
+            cd[i].chi1 = (double *)malloc(sizeof(double) * L->M);
+            cd[i].chi2 = (double *)malloc(sizeof(double) * L->M);
+            orc_chi_table(L, m0, cd[i].chi0);
+            orc_chi_table(L, m0 + 1.0, cd[i].chi1);
+            orc_chi_table(L, m0 + 2.0, cd[i].chi2);
+        }
+    }
+    const int PW = 3 + q + q * q;        /* orc_pair output width */
+    const int K = orc_k_stats(p, q);
+    if (stats) memset(stats, 0, sizeof(double) * ((size_t)g * K + 1));
+    double ll = 0.0;
+    const int64_t CH = 4096;
+    double *buf = (double *)malloc(sizeof(double) * (size_t)CH * g * PW);
+    double *gaps = (double *)malloc(sizeof(double) * (size_t)CH * g);
+    for (int64_t j0 = 0; j0 < n && rc == ORC_OK; j0 += CH) {
+        const int64_t cnt = (n - j0 < CH) ? n - j0 : CH;
+        int prc = ORC_OK;
+#ifdef _OPENMP
+#pragma omp parallel for schedule(dynamic, 1) num_threads(nthreads > 0 ? nthreads : 1)
+#endif
+        for (int64_t jj = 0; jj < cnt * g; ++jj) {
+            const int64_t j = j0 + jj / g;
+            const int i = (int)(jj % g);
+            double gap = INFINITY;
+            const int r2 = orc_pair(p, q, y + (size_t)j * p, mu + (size_t)i * p, cd[i].L, cd[i].A,
+                                    cd[i].Lam, nu[i], cd[i].kappa, L, cd[i].chi0, cd[i].chi1,
+                                    cd[i].chi2, buf + (size_t)jj * PW, &gap);
+            gaps[jj] = gap;
+            if (r2 != ORC_OK) prc = r2;
+        }
+        if (prc != ORC_OK) { rc = prc; break; }
+        for (int64_t jj = 0; jj < cnt; ++jj) {        /* serial, ascending j */
+            const int64_t j = j0 + jj;
+            const double *yj = y + (size_t)j * p;
+            double lf[16], mx = -INFINITY;
+            for (int i = 0; i < g; ++i) {
+                lf[i] = log(pi[i]) + buf[(size_t)(jj * g + i) * PW + 0];
+                if (lf[i] > mx) mx = lf[i];
+            }
+            if (mx == -INFINITY) { rc = ORC_EUNDERFLOW; break; }
+            double se = 0.0;
+            for (int i = 0; i < g; ++i) se += exp(lf[i] - mx);
+            const double lse = mx + log(se);
+            ll += lse;
+            for (int i = 0; i < g; ++i) {
+                const double *o = buf + (size_t)(jj * g + i) * PW;
+                const double tau = exp(lf[i] - lse);
+                if (min_key_gap && gaps[jj * g + i] < min_key_gap[j * g + i]) min_key_gap[j * g + i] = gaps[jj * g + i];
+                if (pair_out) {
+                    double *po = pair_out + ((size_t)j * g + i) * (PW + 1);
+                    po[0] = lf[i];
+                    po[1] = tau;
+                    for (int k = 1; k < PW; ++k) po[1 + k] = o[k];
+                }
+                if (!stats || !(tau > 0.0)) continue;
+                double *S = stats + (size_t)i * K;
+                const double e1me2 = o[1], e2 = o[2];
+                const double *e3 = o + 3, *e4 = o + 3 + q;
+                int off = 0;
+                S[off++] += tau;                                       /* S0 */
+                S[off++] += tau * e2;                                  /* S1 */
+                for (int a = 0; a < p; ++a) S[off++] += tau * e2 * yj[a];               /* S2 */
+                for (int a = 0; a < p; ++a)
+                    for (int b = a; b < p; ++b) S[off++] += tau * e2 * yj[a] * yj[b];   /* S3 */
+                for (int k = 0; k < q; ++k) S[off++] += tau * e3[k];                    /* S4 */
+                for (int k = 0; k < q; ++k)
+                    for (int l = k; l < q; ++l) S[off++] += tau * e4[k * q + l];        /* S5 */
+                for (int a = 0; a < p; ++a)
+                    for (int k = 0; k < q; ++k) S[off++] += tau * yj[a] * e3[k];        /* S6 */
+                S[off++] += tau * e1me2;                               /* S7 */
+            }
+            if (rc != ORC_OK) break;
+        }
+    }
+    if (stats) stats[(size_t)g * K] = ll;
+    if (loglik) *loglik = ll;
+    free(buf);
+    free(gaps);
+    for (int i = 0; i < g; ++i) { free(cd[i].chi0); free(cd[i].chi1); free(cd[i].chi2); }
+    free(cd);
+    return rc;
+}
+
+/* =====================================================================================
+ * M-step (Alg. 3), ECM order (reading A6):
+ *   mu    <- (S2 - Delta_old S4) / S1
+ *   B     <- S6 - mu S4'
+ *   Delta <- B S5^{-1}
+ *   Sigma <- [S3 - S2 mu' - mu S2' + S1 mu mu' - B Delta' - Delta B' + Delta S5 Delta'] / S0
+ *   nu    <- root of log(nu/2) - psi(nu/2) + 1 + S7/S0 on [nu_lo, nu_hi] (reading A7)
+ *   pi    <- S0 / n_total, floored at 1e-10, renormalised
+ * ===================================================================================== */
+static double nu_eq(double nu, double c) { return log(0.5 * nu) - orc_digamma(0.5 * nu) + 1.0 + c; }
+
+int orc_mstep(int p, int q, int g, double n_total, const double *stats,
+              double *pi, double *mu, double *sigma, double *delta, double *nu,
+              double nu_lo, double nu_hi) {
+    const int K = orc_k_stats(p, q);
+    for (int i = 0; i < g; ++i) {
+        const double *S = stats + (size_t)i * K;
+        const double S0 = S[0], S1 = S[1];
+        const double *S2 = S + 2, *S3p = S + 2 + p, *S4 = S3p + p * (p + 1) / 2;
+        const double *S5p = S4 + q, *S6 = S5p + q * (q + 1) / 2;
+        const double S7 = S6[p * q];
+        if (!(S0 >= 1e-10)) return ORC_EEMPTY;
+        double S3[PMAX * PMAX], S5[QMAX * QMAX];
+        int off = 0;
+        for (int a = 0; a < p; ++a)
+            for (int b = a; b < p; ++b) { S3[a * p + b] = S3[b * p + a] = S3p[off++]; }
+        off = 0;
+        for (int k = 0; k < q; ++k)
+            for (int l = k; l < q; ++l) { S5[k * q + l] = S5[l * q + k] = S5p[off++]; }
+        double *mui = mu + (size_t)i * p, *Si = sigma + (size_t)i * p * p, *Di = delta + (size_t)i * p * q;
+        for (int a = 0; a < p; ++a) {
+            double s = S2[a];
+            for (int k = 0; k < q; ++k) s -= Di[a * q + k] * S4[k];
+            mui[a] = s / S1;
+        }
+        double B[PMAX * QMAX];
+        for (int a = 0; a < p; ++a)
+            for (int k = 0; k < q; ++k) B[a * q + k] = S6[a * q + k] - mui[a] * S4[k];
+        if (q > 0) {
+            double L5[QMAX * QMAX];
+            if (chol(q, S5, L5) != ORC_OK) return ORC_ENOTPD;
+            for (int a = 0; a < p; ++a) {
+                double x[QMAX];
+                for (int k = 0; k < q; ++k) x[k] = B[a * q + k];
+                chol_solve(q, L5, x);                                  /* row a of B S5^{-1} */
+                for (int k = 0; k < q; ++k) Di[a * q + k] = x[k];
+            }
+        }
+        for (int a = 0; a < p; ++a)
+            for (int b = 0; b < p; ++b) {
+                double s = S3[a * p + b] - S2[a] * mui[b] - mui[a] * S2[b] + S1 * mui[a] * mui[b];
+                for (int k = 0; k < q; ++k) s -= B[a * q + k] * Di[b * q + k] + Di[a * q + k] * B[b * q + k];
+                for (int k = 0; k < q; ++k)
+                    for (int l = 0; l < q; ++l) s += Di[a * q + k] * S5[k * q + l] * Di[b * q + l];
+                Si[a * p + b] = s / S0;
+            }
+        for (int a = 0; a < p; ++a)
+            for (int b = a + 1; b < p; ++b) {
+                const double s = 0.5 * (Si[a * p + b] + Si[b * p + a]);
+                Si[a * p + b] = Si[b * p + a] = s;
+            }
+        double Lt[PMAX * PMAX];
+        if (chol(p, Si, Lt) != ORC_OK) {                              /* ridge repair */
+            double md = 0.0;
+            for (int a = 0; a < p; ++a) md += Si[a * p + a];
+            md /= p;
+            for (int a = 0; a < p; ++a) Si[a * p + a] += 1e-8 * md;
+            if (chol(p, Si, Lt) != ORC_OK) return ORC_ENOTPD;
+        }
+        /* nu: log(nu/2) - psi(nu/2) decreases from +inf to 0 */
+        const double cst = S7 / S0;
+        if (nu_eq(nu_hi, cst) > 0.0) nu[i] = nu_hi;
+        else if (nu_eq(nu_lo, cst) < 0.0) nu[i] = nu_lo;
+        else {
+            double lo = nu_lo, hi = nu_hi;
+            for (int it = 0; it < 400; ++it) {
+                const double mid = 0.5 * (lo + hi);
+                if (nu_eq(mid, cst) > 0.0) lo = mid; else hi = mid;
+                if (hi - lo <= 1e-12 * 0.5 * (lo + hi)) break;
+            }
+            nu[i] = 0.5 * (lo + hi);
+        }
+    }
+    double tot = 0.0;
+    for (int i = 0; i < g; ++i) {
+        double pv = stats[(size_t)i * K] / n_total;
+        if (pv < 1e-10) pv = 1e-10;
+        pi[i] = pv;
+        tot += pv;
+    }
+    for (int i = 0; i < g; ++i) pi[i] /= tot;
+    return ORC_OK;
+}
+
+/* Alg. 4 with the typo readings of A8 and SPEC.md:338 guards. */
+int orc_aitken_stop(double l_km2, double l_km1, double l_k, double tol) {
+    const double den = l_km1 - l_km2;
+    if (fabs(den) < 1e-300) return 1;
+    const double a = (l_k - l_km1) / den;
+    if (a >= 1.0) return 0;
+    const double linf = l_km1 + (l_k - l_km1) / (1.0 - a);
+    return fabs(linf - l_k) < tol;
+}
+
+/* O13: E-step at Psi^(0) gives l^(0); then [M-step, E-step] per iteration. */
+int orc_fit(int64_t n, int p, int q, int g, const double *y, double *pi, double *mu,
+            double *sigma, double *delta, double *nu, const orc_lattice *L,
+            int nthreads, int max_iter, double tol, double nu_lo, double nu_hi,
+            double *trace, int *n_iter, int *converged) {
+    const int K = orc_k_stats(p, q);
+    double *stats = (double *)malloc(sizeof(double) * ((size_t)g * K + 1));
+    *n_iter = 0;
+    *converged = 0;
+    int rc = orc_estep(n, p, q, g, y, pi, mu, sigma, delta, nu, L, nthreads, NULL, stats, &trace[0], NULL);
+    for (int k = 1; k <= max_iter && rc == ORC_OK; ++k) {
+        rc = orc_mstep(p, q, g, (double)n, stats, pi, mu, sigma, delta, nu, nu_lo, nu_hi);
+        if (rc != ORC_OK) break;
+        rc = orc_estep(n, p, q, g, y, pi, mu, sigma, delta, nu, L, nthreads, NULL, stats, &trace[k], NULL);
+        if (rc != ORC_OK) break;
+        *n_iter = k;
+        if (tol > 0.0 && k >= 2 && orc_aitken_stop(trace[k - 2], trace[k - 1], trace[k], tol)) {
+            *converged = 1;
+            break;
+        }
+    }
+    free(stats);
+    return rc;
+}
