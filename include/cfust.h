@@ -1,0 +1,138 @@
+/*
+ * cfust.h — C ABI of the B200-native FM-CFUST EM hot path (libcfust.so).
+ *
+ * Implements the EM iteration for a g-component mixture of canonical fundamental skew-t
+ * (CFUST) distributions, Eq. (2) of Lee, McLachlan & Leemaqz, arXiv 2005.06848
+ * (PAPER.md:154-166), following the EM outline of PAPER.md:197-226 and the data-parallel
+ * E-step / M-step split of Algorithms 2-3.  The E-/M-step formulas the
+ * paper omits follow DESIGN.md §3 (readings R-E, R-M, R-T).
+ *
+ * Conventions
+ *  - Every call returns int: CFUST_OK (0) or a negative CFUST_E* code; the message is
+ *    available from cfust_last_error(ctx).  Not converging is not an error.
+ *  - All arrays are FP64, row-major, C-contiguous.
+ *  - Host pointers are only read during the call (copied); caller keeps ownership.
+ *    Exception: with opts.y_on_device = 1, y is a DEVICE pointer that the caller owns and
+ *    must keep alive and unchanged until cfust_destroy (it is not copied).
+ *  - The context owns all device memory, its CUDA stream, events and (world > 1) the NCCL
+ *    communicator until cfust_destroy.  No global state; one context per thread at a time.
+ *  - Limits: 1 <= p <= 8, 0 <= q <= 6, 1 <= g <= 8; lattice M a power of two in
+ *    [1024, 65536] when q >= 2 (q <= 1 needs no lattice).
+ *  - There is no CPU fallback: without a CUDA device every call fails with CFUST_ECUDA.
+ */
+#ifndef CFUST_H
+#define CFUST_H
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define CFUST_OK 0
+#define CFUST_EINVAL -1      /* bad argument (NULL, out of range, unsupported M)          */
+#define CFUST_EDIM -2        /* DimensionMismatch (p, q, g, n inconsistent)     */
+#define CFUST_EMIXPROP -3    /* pi_i <= 0 or |sum pi - 1| > 1e-12               */
+#define CFUST_ENOTPD -4      /* Cholesky pivot <= 1e-300 in Sigma, Omega or S5 */
+#define CFUST_EUNDERFLOW -5  /* all g component densities are 0 at some y_j   */
+#define CFUST_EEMPTY -6      /* S0_i < 1e-10: empty component in the M-step    */
+#define CFUST_ECUDA -7       /* CUDA runtime error / no device                               */
+#define CFUST_ENCCL -8       /* NCCL error                                                   */
+
+typedef struct cfust_ctx cfust_ctx;   /* opaque */
+
+/* Mixture parameters Psi = (pi, mu, Sigma, Delta, nu).
+ * Host buffers, caller-owned: pi[g], mu[g][p], sigma[g][p][p] (symmetric PD),
+ * delta[g][p][q] (ignored / may be NULL when q == 0), nu[g] (> 0). */
+typedef struct {
+    double *pi;
+    double *mu;
+    double *sigma;
+    double *delta;
+    double *nu;
+} cfust_params;
+
+/* Options.  Zero-initialise and set what you need. */
+typedef struct {
+    int32_t lattice_m;             /* M: lattice points for T_r, r >= 2 (power of two)           */
+    const uint32_t *lattice_z;     /* [q] rank-1 generating vector (host), reading A12            */
+    const double *lattice_shift;   /* [q] seed-defined shift in (0,1) (host), reading A11          */
+    double nu_lo, nu_hi;           /* nu bracket; 0,0 -> [0.1, 1000] (reading A7)                 */
+    int32_t y_on_device;           /* 1: y is a caller-owned device pointer (not copied)          */
+    int32_t device;                /* CUDA device ordinal; < 0 -> current device                  */
+    int32_t rank, world;           /* world <= 1: single GPU, no NCCL                              */
+    const void *nccl_id;           /* 128-byte ncclUniqueId, identical on all ranks (world > 1)    */
+    int64_t n_total;               /* sum of n over ranks (pi = S0 / n_total); 0 -> n              */
+    int32_t timing;                /* 1: record CUDA events per phase (see cfust_get_timing)       */
+} cfust_opts;
+
+typedef struct {
+    int32_t n_iter;        /* EM iterations (M-steps) performed                              */
+    int32_t converged;     /* 1 if the Aitken rule (Alg. 4) stopped the fit  */
+    double *loglik_trace;  /* caller buffer [trace_cap]: l^(0..n_iter), l^(k) at Psi^(k)      */
+    int32_t trace_cap;
+    double wall_time_s;
+} cfust_result;
+
+/* Create a context on this rank's shard y[n][p] (observations j0..j0+n-1 of the global data;
+ * contiguous blocks), upload Psi^(0) and derive Omega, Lambda, ...
+ * Validates: y finite, pi (EMIXPROP), Sigma/Omega PD (ENOTPD), nu > 0. */
+int cfust_em_init(cfust_ctx **out, const double *y, int64_t n, int32_t p, int32_t g, int32_t q,
+                  const cfust_params *init, const cfust_opts *opts);
+
+/* Replace the data shard (same n, p).  on_device = 0: host array, copied (H2D on the
+ * context stream); 1: caller-owned device pointer, used in place. */
+int cfust_set_data(cfust_ctx *ctx, const double *y, int32_t on_device);
+
+/* E-step at the current Psi^(k) (Eq. (3)-(4), Alg. 2): tau, e1-e2, e2, e3, e4 per pair and the
+ * eight sufficient statistics S0..S7 per component (reading A4), reduced over the shard and
+ * (world > 1) all-reduced over ranks.  loglik_out (may be NULL) receives l^(k) = sum_j log f_j;
+ * stats_out (may be NULL) receives the global vector [g*K + 1], K = cfust_k_stats(p, q):
+ * per component [S0, S1, S2(p), S3(p(p+1)/2, upper row-major), S4(q), S5(q(q+1)/2),
+ * S6(p*q row-major), S7], then l.  Blocks until the results are on the host if either is non-NULL. */
+int cfust_estep(cfust_ctx *ctx, double *loglik_out, double *stats_out);
+
+/* M-step (Alg. 3; reading R-M, ECM order) from the last E-step's statistics, entirely on the
+ * device: mu, Delta, Sigma, nu (bisection root), pi; then re-derives Omega, Lambda, chi nodes. */
+int cfust_mstep(cfust_ctx *ctx);
+
+/* One EM iteration = cfust_estep + cfust_mstep; *loglik_out = l at the pre-M-step Psi. */
+int cfust_iterate(cfust_ctx *ctx, double *loglik_out);
+
+/* Density-only pass (T0 only): l = sum_j log f(y_j; Psi) at the current Psi (Eq. (3)). */
+int cfust_loglik(cfust_ctx *ctx, double *out);
+
+/* Full fit: E-step, then max_iter x [M-step, E-step] with the Aitken stop when tol > 0
+ * (Alg. 4, reading A8); out->loglik_trace gets l^(0..n_iter). */
+int cfust_fit(cfust_ctx *ctx, int32_t max_iter, double tol, cfust_result *out);
+
+int cfust_get_params(cfust_ctx *ctx, cfust_params *out);         /* copies into caller buffers */
+int cfust_set_params(cfust_ctx *ctx, const cfust_params *in);    /* validates, re-derives      */
+
+/* Per-pair E-step outputs for observations idx[0..cnt) (local indices) at the current Psi,
+ * for parity checks: out[cnt][g][4 + q + q*q] = log(pi_i f_ij), tau_ij, e1-e2, e2, e3(q), e4(q*q).
+ * Does not touch the accumulated statistics. */
+int cfust_get_pairs(cfust_ctx *ctx, const int64_t *idx, int64_t cnt, double *out);
+
+/* Accumulated device time per phase since the last reset (opts.timing = 1):
+ * ms[0] E-step kernel, ms[1] reduce, ms[2] all-reduce, ms[3] M-step+derive+chi nodes;
+ * counts[0..3] launches per phase.  reset != 0 clears after reading. */
+int cfust_get_timing(cfust_ctx *ctx, double *ms, int64_t *counts, int32_t reset);
+
+/* The cudaStream_t the context launches on (as void*), for event timing by the caller. */
+void *cfust_stream(cfust_ctx *ctx);
+
+/* Kernel launches issued since creation (for bench's gpu_launches). */
+int64_t cfust_launch_count(cfust_ctx *ctx);
+
+/* Fill out[128] with a fresh ncclUniqueId (rank 0), to be broadcast to all ranks and passed
+ * as opts.nccl_id (one NCCL all-reduce of the statistics per iteration). */
+int cfust_nccl_unique_id(void *out);
+
+int cfust_k_stats(int32_t p, int32_t q);
+const char *cfust_last_error(const cfust_ctx *ctx);
+void cfust_destroy(cfust_ctx *ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CFUST_H */

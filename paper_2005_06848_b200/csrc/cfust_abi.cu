@@ -1,0 +1,526 @@
+// cfust_abi.cu — host side of libcfust.so: context, validation, NCCL, and the C ABI
+// declared in include/cfust.h.  Every step of the hot path runs in cfust_kernels.cu; this
+// file only allocates, launches, and moves the O(g K) statistics vector.
+#include "cfust.h"
+#include "cfust_device.cuh"
+#include "cfust_internal.h"
+
+#include <nccl.h>
+
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+using namespace cfust;
+
+struct cfust_ctx {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    DevState s{};
+    double *y_owned = nullptr;
+    double *d_ll = nullptr;        // loglik-only result
+    double *h_pin = nullptr;       // pinned: [0] loglik, [1..] stats staging
+    int *h_status = nullptr;       // pinned [4]
+    ncclComm_t comm = nullptr;
+    int world = 1, rank = 0;
+    bool have_stats = false;
+    bool timing = false;
+    cudaEvent_t ev[5] = {};
+    double ms[4] = {0, 0, 0, 0};
+    int64_t counts[4] = {0, 0, 0, 0};
+    int64_t launches = 0;
+    int nblocks_last = 0;
+    std::string err;
+};
+
+namespace {
+
+int fail(cfust_ctx *c, int code, const std::string &msg) {
+    if (c) c->err = msg;
+    return code;
+}
+
+#define CU(call)                                                                                        \
+    do {                                                                                                \
+        cudaError_t e_ = (call);                                                                        \
+        if (e_ != cudaSuccess) return fail(ctx, CFUST_ECUDA, std::string(#call) + ": " + cudaGetErrorString(e_)); \
+    } while (0)
+
+#define CUI(call)                                                                                       \
+    do {                                                                                                \
+        int e_ = (call);                                                                                \
+        if (e_ != 0) return fail(ctx, CFUST_ECUDA, std::string(#call) + ": " + cudaGetErrorString(cudaError_t(e_))); \
+    } while (0)
+
+#define NC(call)                                                                                        \
+    do {                                                                                                \
+        ncclResult_t r_ = (call);                                                                       \
+        if (r_ != ncclSuccess) return fail(ctx, CFUST_ENCCL, std::string(#call) + ": " + ncclGetErrorString(r_)); \
+    } while (0)
+
+int k_stats(int p, int q) { return 3 + p + p * (p + 1) / 2 + q + q * (q + 1) / 2 + p * q; }
+
+// Host-side validation of Psi.
+int validate_params(cfust_ctx *ctx, int p, int q, int g, const cfust_params *P) {
+    if (!P || !P->pi || !P->mu || !P->sigma || !P->nu || (q > 0 && !P->delta))
+        return fail(ctx, CFUST_EINVAL, "NULL parameter array");
+    double tot = 0.0;
+    for (int i = 0; i < g; ++i) {
+        if (!(P->pi[i] > 0.0)) return fail(ctx, CFUST_EMIXPROP, "pi_i <= 0");
+        tot += P->pi[i];
+        if (!(P->nu[i] > 0.0) || !std::isfinite(P->nu[i])) return fail(ctx, CFUST_EINVAL, "nu_i must be > 0");
+    }
+    if (!(std::fabs(tot - 1.0) <= 1e-12)) return fail(ctx, CFUST_EMIXPROP, "|sum pi - 1| > 1e-12");
+    for (int t = 0; t < g * p; ++t)
+        if (!std::isfinite(P->mu[t])) return fail(ctx, CFUST_EINVAL, "mu not finite");
+    for (int i = 0; i < g; ++i)
+        for (int a = 0; a < p; ++a)
+            for (int b = 0; b < p; ++b) {
+                const double x = P->sigma[(size_t(i) * p + a) * p + b], y = P->sigma[(size_t(i) * p + b) * p + a];
+                if (!std::isfinite(x)) return fail(ctx, CFUST_EINVAL, "Sigma not finite");
+                if (std::fabs(x - y) > 1e-12 * (std::fabs(x) + std::fabs(y) + 1e-300))
+                    return fail(ctx, CFUST_EDIM, "Sigma not symmetric");
+            }
+    for (int t = 0; t < g * p * q; ++t)
+        if (!std::isfinite(P->delta[t])) return fail(ctx, CFUST_EINVAL, "Delta not finite");
+    return CFUST_OK;
+}
+
+int upload_params(cfust_ctx *ctx, const cfust_params *P) {
+    DevState &s = ctx->s;
+    const int p = s.p, q = s.q, g = s.g;
+    CU(cudaMemcpyAsync(s.pi, P->pi, sizeof(double) * g, cudaMemcpyHostToDevice, ctx->stream));
+    CU(cudaMemcpyAsync(s.mu, P->mu, sizeof(double) * g * p, cudaMemcpyHostToDevice, ctx->stream));
+    CU(cudaMemcpyAsync(s.sigma, P->sigma, sizeof(double) * g * p * p, cudaMemcpyHostToDevice, ctx->stream));
+    if (q > 0) CU(cudaMemcpyAsync(s.delta, P->delta, sizeof(double) * g * p * q, cudaMemcpyHostToDevice, ctx->stream));
+    CU(cudaMemcpyAsync(s.nu, P->nu, sizeof(double) * g, cudaMemcpyHostToDevice, ctx->stream));
+    return CFUST_OK;
+}
+
+// status word -> error code (after a stream sync)
+int check_status(cfust_ctx *ctx) {
+    const int *st = ctx->h_status;
+    if (st[1] < 0) {
+        const int code = st[1];
+        return fail(ctx, code, code == CFUST_ENOTPD ? "matrix not positive definite (Cholesky pivot <= 1e-300)"
+                               : code == CFUST_EEMPTY ? "empty component: S0_i < 1e-10"
+                                                      : "M-step/derive error");
+    }
+    if (st[0] & 1) return fail(ctx, CFUST_EUNDERFLOW, "all component densities underflow at some observation");
+    if (st[2]) return fail(ctx, CFUST_EINVAL, "y has non-finite entries");
+    return CFUST_OK;
+}
+
+int fetch_status_and_sync(cfust_ctx *ctx) {
+    CU(cudaMemcpyAsync(ctx->h_status, ctx->s.status, sizeof(int) * 4, cudaMemcpyDeviceToHost, ctx->stream));
+    CU(cudaStreamSynchronize(ctx->stream));
+    return check_status(ctx);
+}
+
+void rec(cfust_ctx *ctx, int k) {
+    if (ctx->timing) cudaEventRecord(ctx->ev[k], ctx->stream);
+}
+
+void acc_phase(cfust_ctx *ctx, int a, int b, int slot) {
+    if (!ctx->timing) return;
+    float t = 0.f;
+    if (cudaEventElapsedTime(&t, ctx->ev[a], ctx->ev[b]) == cudaSuccess) {
+        ctx->ms[slot] += t;
+        ctx->counts[slot] += 1;
+    }
+}
+
+int reset_status(cfust_ctx *ctx) {
+    CU(cudaMemsetAsync(ctx->s.status, 0, sizeof(int) * 4, ctx->stream));
+    return CFUST_OK;
+}
+
+// E-step (mode 0) or loglik (mode 1) up to the global reduction; no host sync.
+int enqueue_estep(cfust_ctx *ctx, int mode) {
+    DevState &s = ctx->s;
+    int nb = 0;
+    rec(ctx, 0);
+    CUI(launch_estep(s, mode, nullptr, 0, nullptr, ctx->stream, &nb));
+    ctx->launches += 1;
+    rec(ctx, 1);
+    CUI(launch_reduce(s, nb, mode, mode == 1 ? ctx->d_ll : s.stats, ctx->stream));
+    ctx->launches += 1;
+    rec(ctx, 2);
+    ctx->nblocks_last = nb;
+    if (ctx->world > 1) {
+        const size_t len = (mode == 1) ? 1 : size_t(s.g) * s.K + 1;
+        NC(ncclAllReduce(mode == 1 ? ctx->d_ll : s.stats, mode == 1 ? ctx->d_ll : s.stats, len, ncclDouble, ncclSum,
+                         ctx->comm, ctx->stream));
+    }
+    rec(ctx, 3);
+    return CFUST_OK;
+}
+
+int enqueue_mstep(cfust_ctx *ctx) {
+    CUI(launch_mstep(ctx->s, ctx->stream));
+    CUI(launch_chi(ctx->s, ctx->stream));
+    ctx->launches += (ctx->s.q >= 2) ? 2 : 1;
+    rec(ctx, 4);
+    return CFUST_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int cfust_k_stats(int32_t p, int32_t q) { return k_stats(p, q); }
+
+int cfust_nccl_unique_id(void *out) {
+    if (!out) return CFUST_EINVAL;
+    ncclUniqueId id;
+    if (ncclGetUniqueId(&id) != ncclSuccess) return CFUST_ENCCL;
+    std::memcpy(out, &id, sizeof(id));
+    return CFUST_OK;
+}
+
+const char *cfust_last_error(const cfust_ctx *ctx) { return ctx ? ctx->err.c_str() : "NULL context"; }
+
+void *cfust_stream(cfust_ctx *ctx) { return ctx ? (void *)ctx->stream : nullptr; }
+
+int64_t cfust_launch_count(cfust_ctx *ctx) { return ctx ? ctx->launches : 0; }
+
+void cfust_destroy(cfust_ctx *ctx) {
+    if (!ctx) return;
+    if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+    if (ctx->comm) ncclCommDestroy(ctx->comm);
+    DevState &s = ctx->s;
+    cudaFree(ctx->y_owned);
+    cudaFree(s.pi);
+    cudaFree(s.mu);
+    cudaFree(s.sigma);
+    cudaFree(s.delta);
+    cudaFree(s.nu);
+    cudaFree(s.comp);
+    cudaFree(s.chi);
+    cudaFree(s.partials);
+    cudaFree(s.stats);
+    cudaFree(s.status);
+    cudaFree(ctx->d_ll);
+    cudaFreeHost(ctx->h_pin);
+    cudaFreeHost(ctx->h_status);
+    for (auto &e : ctx->ev)
+        if (e) cudaEventDestroy(e);
+    if (ctx->stream) cudaStreamDestroy(ctx->stream);
+    delete ctx;
+}
+
+int cfust_em_init(cfust_ctx **out, const double *y, int64_t n, int32_t p, int32_t g, int32_t q,
+                  const cfust_params *init, const cfust_opts *opts) {
+    if (!out) return CFUST_EINVAL;
+    *out = nullptr;
+    cfust_ctx *ctx = new cfust_ctx();
+    int rc = CFUST_OK;
+    do {
+        if (!opts) { rc = fail(ctx, CFUST_EINVAL, "opts is NULL"); break; }
+        if (p < 1 || p > PMAX || q < 0 || q > QMAX || g < 1 || g > GMAX || n < 0) {
+            rc = fail(ctx, CFUST_EDIM, "need 1<=p<=8, 0<=q<=6, 1<=g<=8, n>=0");
+            break;
+        }
+        if (n > 0 && !y) { rc = fail(ctx, CFUST_EINVAL, "y is NULL"); break; }
+        const int M = (q >= 2) ? opts->lattice_m : 0;
+        if (q >= 2) {
+            if (M < 1024 || M > 65536 || (M & (M - 1)) != 0) {
+                rc = fail(ctx, CFUST_EINVAL, "lattice_m must be a power of two in [1024, 65536]");
+                break;
+            }
+            if (!opts->lattice_z || !opts->lattice_shift) { rc = fail(ctx, CFUST_EINVAL, "lattice z/shift NULL"); break; }
+            for (int k = 0; k < q; ++k) {
+                if (opts->lattice_z[k] == 0 || opts->lattice_z[k] >= uint32_t(M)) { rc = fail(ctx, CFUST_EINVAL, "bad lattice z"); break; }
+                if (!(opts->lattice_shift[k] > 0.0 && opts->lattice_shift[k] < 1.0)) { rc = fail(ctx, CFUST_EINVAL, "lattice shift must be in (0,1)"); break; }
+            }
+            if (rc != CFUST_OK) break;
+        }
+        rc = validate_params(ctx, p, q, g, init);
+        if (rc != CFUST_OK) break;
+        ctx->world = opts->world > 1 ? opts->world : 1;
+        ctx->rank = opts->rank;
+        ctx->timing = opts->timing != 0;
+        int ndev = 0;
+        if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev < 1) { rc = fail(ctx, CFUST_ECUDA, "no CUDA device"); break; }
+        ctx->device = opts->device >= 0 ? opts->device : 0;
+        if (opts->device < 0) cudaGetDevice(&ctx->device);
+        if (cudaSetDevice(ctx->device) != cudaSuccess) { rc = fail(ctx, CFUST_ECUDA, "cudaSetDevice failed"); break; }
+        cudaDeviceProp prop;
+        if (cudaGetDeviceProperties(&prop, ctx->device) != cudaSuccess) { rc = fail(ctx, CFUST_ECUDA, "cudaGetDeviceProperties"); break; }
+        if (prop.major < 10) { rc = fail(ctx, CFUST_ECUDA, "libcfust is built for sm_100a (B200)"); break; }
+        if (cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) != cudaSuccess) { rc = fail(ctx, CFUST_ECUDA, "stream"); break; }
+        for (auto &e : ctx->ev)
+            if (cudaEventCreate(&e) != cudaSuccess) { rc = fail(ctx, CFUST_ECUDA, "event"); break; }
+        if (rc != CFUST_OK) break;
+        DevState &s = ctx->s;
+        s.p = p; s.q = q; s.g = g; s.K = k_stats(p, q);
+        s.n = n;
+        s.n_total = opts->n_total > 0 ? double(opts->n_total) : double(n);
+        s.nu_lo = (opts->nu_lo > 0.0) ? opts->nu_lo : 0.1;
+        s.nu_hi = (opts->nu_hi > 0.0) ? opts->nu_hi : 1000.0;
+        s.M = M;
+        for (int k = 0; k < 8; ++k) { s.z[k] = 1; s.shift[k] = 0.5; }
+        for (int k = 0; k < q && M > 0; ++k) { s.z[k] = opts->lattice_z[k]; s.shift[k] = opts->lattice_shift[k]; }
+        s.num_sms = prop.multiProcessorCount;
+        const int GK1 = g * s.K + 1;
+        auto alloc = [&](void **ptr, size_t bytes) { return cudaMalloc(ptr, bytes < 8 ? 8 : bytes) == cudaSuccess; };
+        bool ok = alloc((void **)&s.pi, sizeof(double) * g) && alloc((void **)&s.mu, sizeof(double) * g * p) &&
+                  alloc((void **)&s.sigma, sizeof(double) * g * p * p) &&
+                  alloc((void **)&s.delta, sizeof(double) * g * p * (q > 0 ? q : 1)) &&
+                  alloc((void **)&s.nu, sizeof(double) * g) && alloc((void **)&s.comp, comp_dev_size() * g) &&
+                  alloc((void **)&s.chi, sizeof(double) * g * 3 * (M > 0 ? M : 1)) &&
+                  alloc((void **)&s.partials, sizeof(double) * size_t(max_partial_blocks(s)) * GK1) &&
+                  alloc((void **)&s.stats, sizeof(double) * GK1) && alloc((void **)&s.status, sizeof(int) * 4) &&
+                  alloc((void **)&ctx->d_ll, sizeof(double));
+        if (!ok) { rc = fail(ctx, CFUST_ECUDA, "cudaMalloc failed"); break; }
+        if (cudaMallocHost((void **)&ctx->h_pin, sizeof(double) * (GK1 + 2)) != cudaSuccess ||
+            cudaMallocHost((void **)&ctx->h_status, sizeof(int) * 4) != cudaSuccess) {
+            rc = fail(ctx, CFUST_ECUDA, "cudaMallocHost failed");
+            break;
+        }
+        if (opts->y_on_device) {
+            s.y = y;
+        } else {
+            if (cudaMalloc((void **)&ctx->y_owned, sizeof(double) * (n > 0 ? n * p : 1)) != cudaSuccess) {
+                rc = fail(ctx, CFUST_ECUDA, "cudaMalloc y failed");
+                break;
+            }
+            if (n > 0 && cudaMemcpyAsync(ctx->y_owned, y, sizeof(double) * n * p, cudaMemcpyHostToDevice, ctx->stream) != cudaSuccess) {
+                rc = fail(ctx, CFUST_ECUDA, "copy y failed");
+                break;
+            }
+            s.y = ctx->y_owned;
+        }
+        rc = reset_status(ctx);
+        if (rc != CFUST_OK) break;
+        rc = upload_params(ctx, init);
+        if (rc != CFUST_OK) break;
+        if (launch_check_finite(s.y, n * p, s.status + 2, ctx->stream) != 0 || launch_derive(s, ctx->stream) != 0 ||
+            launch_chi(s, ctx->stream) != 0) {
+            rc = fail(ctx, CFUST_ECUDA, cudaGetErrorString(cudaGetLastError()));
+            break;
+        }
+        ctx->launches += 3;
+        rc = fetch_status_and_sync(ctx);
+        if (rc != CFUST_OK) break;
+        if (ctx->world > 1) {
+            if (!opts->nccl_id) { rc = fail(ctx, CFUST_EINVAL, "world > 1 needs nccl_id"); break; }
+            ncclUniqueId id;
+            std::memcpy(&id, opts->nccl_id, sizeof(id));
+            ncclResult_t r = ncclCommInitRank(&ctx->comm, ctx->world, id, ctx->rank);
+            if (r != ncclSuccess) { rc = fail(ctx, CFUST_ENCCL, std::string("ncclCommInitRank: ") + ncclGetErrorString(r)); break; }
+        }
+    } while (0);
+    if (rc != CFUST_OK) {
+        // keep the message retrievable: return a context only on success; print for the caller
+        std::fprintf(stderr, "cfust_em_init: %s\n", ctx->err.c_str());
+        cfust_destroy(ctx);
+        return rc;
+    }
+    *out = ctx;
+    return CFUST_OK;
+}
+
+int cfust_set_data(cfust_ctx *ctx, const double *y, int32_t on_device) {
+    if (!ctx || !y) return CFUST_EINVAL;
+    DevState &s = ctx->s;
+    if (on_device) {
+        s.y = y;
+    } else {
+        if (!ctx->y_owned) CU(cudaMalloc((void **)&ctx->y_owned, sizeof(double) * (s.n > 0 ? s.n * s.p : 1)));
+        if (s.n > 0) CU(cudaMemcpyAsync(ctx->y_owned, y, sizeof(double) * s.n * s.p, cudaMemcpyHostToDevice, ctx->stream));
+        s.y = ctx->y_owned;
+    }
+    return CFUST_OK;
+}
+
+int cfust_estep(cfust_ctx *ctx, double *loglik_out, double *stats_out) {
+    if (!ctx) return CFUST_EINVAL;
+    CU(cudaSetDevice(ctx->device));
+    DevState &s = ctx->s;
+    int rc = reset_status(ctx);
+    if (rc) return rc;
+    rc = enqueue_estep(ctx, 0);
+    if (rc) return rc;
+    const size_t len = size_t(s.g) * s.K + 1;
+    CU(cudaMemcpyAsync(ctx->h_pin, s.stats, sizeof(double) * len, cudaMemcpyDeviceToHost, ctx->stream));
+    rc = fetch_status_and_sync(ctx);
+    acc_phase(ctx, 0, 1, 0);
+    acc_phase(ctx, 1, 2, 1);
+    acc_phase(ctx, 2, 3, 2);
+    ctx->have_stats = (rc == CFUST_OK);
+    if (rc) return rc;
+    if (loglik_out) *loglik_out = ctx->h_pin[len - 1];
+    if (stats_out) std::memcpy(stats_out, ctx->h_pin, sizeof(double) * len);
+    return CFUST_OK;
+}
+
+int cfust_mstep(cfust_ctx *ctx) {
+    if (!ctx) return CFUST_EINVAL;
+    if (!ctx->have_stats) return fail(ctx, CFUST_EINVAL, "cfust_mstep needs a preceding cfust_estep");
+    CU(cudaSetDevice(ctx->device));
+    int rc = reset_status(ctx);
+    if (rc) return rc;
+    rec(ctx, 3);
+    rc = enqueue_mstep(ctx);
+    if (rc) return rc;
+    rc = fetch_status_and_sync(ctx);
+    acc_phase(ctx, 3, 4, 3);
+    ctx->have_stats = false;
+    return rc;
+}
+
+int cfust_iterate(cfust_ctx *ctx, double *loglik_out) {
+    if (!ctx) return CFUST_EINVAL;
+    CU(cudaSetDevice(ctx->device));
+    DevState &s = ctx->s;
+    int rc = reset_status(ctx);
+    if (rc) return rc;
+    rc = enqueue_estep(ctx, 0);
+    if (rc) return rc;
+    const size_t len = size_t(s.g) * s.K + 1;
+    // l^(k) lives in stats[len-1]; copy it before the M-step (the M-step does not modify stats)
+    CU(cudaMemcpyAsync(ctx->h_pin, s.stats + (len - 1), sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    rc = enqueue_mstep(ctx);
+    if (rc) return rc;
+    rc = fetch_status_and_sync(ctx);
+    acc_phase(ctx, 0, 1, 0);
+    acc_phase(ctx, 1, 2, 1);
+    acc_phase(ctx, 2, 3, 2);
+    acc_phase(ctx, 3, 4, 3);
+    ctx->have_stats = false;
+    if (rc) return rc;
+    if (loglik_out) *loglik_out = ctx->h_pin[0];
+    return CFUST_OK;
+}
+
+int cfust_loglik(cfust_ctx *ctx, double *out) {
+    if (!ctx || !out) return CFUST_EINVAL;
+    CU(cudaSetDevice(ctx->device));
+    int rc = reset_status(ctx);
+    if (rc) return rc;
+    rc = enqueue_estep(ctx, 1);
+    if (rc) return rc;
+    CU(cudaMemcpyAsync(ctx->h_pin, ctx->d_ll, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    rc = fetch_status_and_sync(ctx);
+    if (rc) return rc;
+    *out = ctx->h_pin[0];
+    return CFUST_OK;
+}
+
+static int aitken_stop(double l2, double l1, double l0, double tol) {
+    const double den = l1 - l2;
+    if (std::fabs(den) < 1e-300) return 1;
+    const double a = (l0 - l1) / den;
+    if (a >= 1.0) return 0;
+    const double linf = l1 + (l0 - l1) / (1.0 - a);
+    return std::fabs(linf - l0) < tol;
+}
+
+int cfust_fit(cfust_ctx *ctx, int32_t max_iter, double tol, cfust_result *out) {
+    if (!ctx || !out || max_iter < 0) return CFUST_EINVAL;
+    if (out->loglik_trace && out->trace_cap < max_iter + 1) return fail(ctx, CFUST_EINVAL, "trace_cap < max_iter + 1");
+    const auto t0 = std::chrono::steady_clock::now();
+    std::vector<double> tr;
+    tr.reserve(size_t(max_iter) + 1);
+    double l = 0.0;
+    int rc = cfust_estep(ctx, &l, nullptr);
+    if (rc) return rc;
+    tr.push_back(l);
+    out->n_iter = 0;
+    out->converged = 0;
+    for (int k = 1; k <= max_iter; ++k) {
+        rc = cfust_mstep(ctx);
+        if (rc) break;
+        rc = cfust_estep(ctx, &l, nullptr);   // E-step at Psi^(k) yields l^(k) (trace convention)
+        if (rc) break;
+        tr.push_back(l);
+        out->n_iter = k;
+        if (tol > 0.0 && k >= 2 && aitken_stop(tr[k - 2], tr[k - 1], tr[k], tol)) {
+            out->converged = 1;
+            break;
+        }
+    }
+    if (out->loglik_trace)
+        for (size_t k = 0; k < tr.size() && int(k) < out->trace_cap; ++k) out->loglik_trace[k] = tr[k];
+    out->wall_time_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    return rc;
+}
+
+int cfust_get_params(cfust_ctx *ctx, cfust_params *P) {
+    if (!ctx || !P || !P->pi || !P->mu || !P->sigma || !P->nu) return CFUST_EINVAL;
+    DevState &s = ctx->s;
+    CU(cudaSetDevice(ctx->device));
+    CU(cudaMemcpyAsync(P->pi, s.pi, sizeof(double) * s.g, cudaMemcpyDeviceToHost, ctx->stream));
+    CU(cudaMemcpyAsync(P->mu, s.mu, sizeof(double) * s.g * s.p, cudaMemcpyDeviceToHost, ctx->stream));
+    CU(cudaMemcpyAsync(P->sigma, s.sigma, sizeof(double) * s.g * s.p * s.p, cudaMemcpyDeviceToHost, ctx->stream));
+    if (s.q > 0 && P->delta)
+        CU(cudaMemcpyAsync(P->delta, s.delta, sizeof(double) * s.g * s.p * s.q, cudaMemcpyDeviceToHost, ctx->stream));
+    CU(cudaMemcpyAsync(P->nu, s.nu, sizeof(double) * s.g, cudaMemcpyDeviceToHost, ctx->stream));
+    CU(cudaStreamSynchronize(ctx->stream));
+    return CFUST_OK;
+}
+
+int cfust_set_params(cfust_ctx *ctx, const cfust_params *P) {
+    if (!ctx) return CFUST_EINVAL;
+    DevState &s = ctx->s;
+    int rc = validate_params(ctx, s.p, s.q, s.g, P);
+    if (rc) return rc;
+    CU(cudaSetDevice(ctx->device));
+    rc = reset_status(ctx);
+    if (rc) return rc;
+    rc = upload_params(ctx, P);
+    if (rc) return rc;
+    CUI(launch_derive(s, ctx->stream));
+    CUI(launch_chi(s, ctx->stream));
+    ctx->launches += 2;
+    ctx->have_stats = false;
+    return fetch_status_and_sync(ctx);
+}
+
+int cfust_get_pairs(cfust_ctx *ctx, const int64_t *idx, int64_t cnt, double *out) {
+    if (!ctx || cnt < 0 || (cnt > 0 && (!idx || !out))) return CFUST_EINVAL;
+    if (cnt == 0) return CFUST_OK;
+    DevState &s = ctx->s;
+    for (int64_t k = 0; k < cnt; ++k)
+        if (idx[k] < 0 || idx[k] >= s.n) return fail(ctx, CFUST_EINVAL, "pair index out of range");
+    CU(cudaSetDevice(ctx->device));
+    const size_t PW = size_t(4 + s.q + s.q * s.q);
+    int64_t *d_idx = nullptr;
+    double *d_out = nullptr;
+    CU(cudaMalloc((void **)&d_idx, sizeof(int64_t) * cnt));
+    if (cudaMalloc((void **)&d_out, sizeof(double) * cnt * s.g * PW) != cudaSuccess) {
+        cudaFree(d_idx);
+        return fail(ctx, CFUST_ECUDA, "cudaMalloc pair_out");
+    }
+    int rc = reset_status(ctx);
+    int nb = 0;
+    if (!rc && cudaMemcpyAsync(d_idx, idx, sizeof(int64_t) * cnt, cudaMemcpyHostToDevice, ctx->stream) != cudaSuccess)
+        rc = fail(ctx, CFUST_ECUDA, "copy idx");
+    if (!rc && launch_estep(s, 2, d_idx, cnt, d_out, ctx->stream, &nb) != 0)
+        rc = fail(ctx, CFUST_ECUDA, cudaGetErrorString(cudaGetLastError()));
+    ctx->launches += 1;
+    if (!rc && cudaMemcpyAsync(out, d_out, sizeof(double) * cnt * s.g * PW, cudaMemcpyDeviceToHost, ctx->stream) != cudaSuccess)
+        rc = fail(ctx, CFUST_ECUDA, "copy pair_out");
+    if (!rc) rc = fetch_status_and_sync(ctx);
+    cudaStreamSynchronize(ctx->stream);
+    cudaFree(d_idx);
+    cudaFree(d_out);
+    return rc;
+}
+
+int cfust_get_timing(cfust_ctx *ctx, double *ms, int64_t *counts, int32_t reset) {
+    if (!ctx) return CFUST_EINVAL;
+    for (int k = 0; k < 4; ++k) {
+        if (ms) ms[k] = ctx->ms[k];
+        if (counts) counts[k] = ctx->counts[k];
+    }
+    if (reset)
+        for (int k = 0; k < 4; ++k) { ctx->ms[k] = 0; ctx->counts[k] = 0; }
+    return CFUST_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,190 @@
+// cfust_device.cuh — device-side data layout and FP64 special functions (sm_100a).
+//
+// Independent of oracle/ (no shared code): written for the GPU from the same mathematical
+// definitions.  Cites: Eq. (2) PAPER.md:154-166.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+#include <math_constants.h>
+
+namespace cfust {
+
+constexpr int PMAX = 8;
+constexpr int QMAX = 6;
+constexpr int GMAX = 8;
+constexpr double UMIN = 1e-300;                 // SOV clamp (reading A15)
+constexpr double UMAX = 0x1.fffffffffffffp-1;   // largest double below 1
+
+// Per-component quantities derived from Psi, recomputed after each M-step.
+struct CompDev {
+    double mu[PMAX];
+    double L[PMAX * PMAX];        // chol(Omega), lower, row-major p x p (stride PMAX)
+    double Linv[PMAX];            // 1 / L_aa
+    double A[QMAX * PMAX];        // Delta' Omega^{-1}, q x p (stride PMAX)
+    double Lam[QMAX * QMAX];      // Lambda = I - Delta' Omega^{-1} Delta, q x q (stride QMAX)
+    double nu, m0, kappa, logpi;  // kappa = log t_p normaliser incl. -1/2 log|Omega|
+    double psi_half_m0;           // digamma(m0/2) for e1 - e2 (reading A5)
+    double lgc_m0;                // lgamma((m0+1)/2) - lgamma(m0/2)      (t_1 density, df m0)
+    double lgc_m0m1;              // lgamma(m0/2) - lgamma((m0-1)/2)      (t_1 density, df m0-1)
+    double pad;
+};
+
+struct LatticeDev {
+    int M;                        // power of two
+    uint32_t z[QMAX];
+    double shift[QMAX];
+};
+
+// ------------------------------------------------------------------------------------------
+// Lattice point coordinate k of point l:  x = frac((l z_k mod M)/M + shift_k), w = |2x - 1|
+// (reading A11, tent periodisation).  (l z_k mod M)/M and 2x are exact in FP64.
+__device__ __forceinline__ double lattice_w(const LatticeDev& L, int l, int k) {
+    const uint32_t t = (uint32_t(l) * L.z[k]) & uint32_t(L.M - 1);
+    double x = __dadd_rn(__dmul_rn(double(t), 1.0 / double(L.M)), L.shift[k]);
+    if (x >= 1.0) x -= 1.0;
+    return fabs(__dadd_rn(__dmul_rn(2.0, x), -1.0));
+}
+
+// ------------------------------------------------------------------------------------------
+// Standard normal CDF / quantile (CUDA libdevice, FP64).
+__device__ __forceinline__ double Phi(double x) { return normcdf(x); }
+__device__ __forceinline__ double Phiinv(double u) { return normcdfinv(u); }
+
+// digamma: upward recurrence to x >= 16, then the Stirling-type asymptotic series.
+__device__ inline double dev_digamma(double x) {
+    double acc = 0.0;
+    while (x < 16.0) { acc += 1.0 / x; x += 1.0; }
+    const double r = 1.0 / x, r2 = r * r;
+    const double ser = r2 * (1.0 / 12 - r2 * (1.0 / 120 - r2 * (1.0 / 252 - r2 * (1.0 / 240 - r2 * (1.0 / 132)))));
+    return log(x) - 0.5 * r - ser - acc;
+}
+
+// Continued fraction of the regularized incomplete beta (modified Lentz):
+//   I_x(a,b) = x^a (1-x)^b / (a B(a,b)) * cf(a,b,x),  converging fast for x < (a+1)/(a+b+2).
+__device__ inline double dev_betacf(double a, double b, double x) {
+    const double fpmin = 1e-300;
+    double c = 1.0;
+    double d = 1.0 - (a + b) * x / (a + 1.0);
+    d = (fabs(d) < fpmin) ? fpmin : d;
+    d = 1.0 / d;
+    double h = d;
+    for (int m = 1; m <= 4000; ++m) {
+        const double m2 = 2.0 * m;
+        const double num_e = m * (b - m) * x / ((a + m2 - 1.0) * (a + m2));
+        d = 1.0 + num_e * d; d = (fabs(d) < fpmin) ? fpmin : d; d = 1.0 / d;
+        c = 1.0 + num_e / c; c = (fabs(c) < fpmin) ? fpmin : c;
+        h *= d * c;
+        const double num_o = -(a + m) * (a + b + m) * x / ((a + m2) * (a + m2 + 1.0));
+        d = 1.0 + num_o * d; d = (fabs(d) < fpmin) ? fpmin : d; d = 1.0 / d;
+        c = 1.0 + num_o / c; c = (fabs(c) < fpmin) ? fpmin : c;
+        const double del = d * c;
+        h *= del;
+        if (fabs(del - 1.0) <= 1e-16) break;
+    }
+    return h;
+}
+
+// Univariate Student-t CDF with real df m:  P(T <= t) = 1 - I_{m/(m+t^2)}(m/2, 1/2)/2 for t >= 0.
+__device__ inline double dev_t_cdf(double t, double m) {
+    if (isinf(t)) return t > 0 ? 1.0 : 0.0;
+    const double t2 = t * t;
+    const double x = m / (m + t2), xc = t2 / (m + t2);
+    const double a = 0.5 * m, b = 0.5;
+    const double lbeta = lgamma(a) + lgamma(b) - lgamma(a + b);
+    const double lx = (x > 0.5) ? log1p(-xc) : log(x);
+    const double lxc = (xc > 0.5) ? log1p(-x) : log(xc);
+    const double front = exp(a * lx + b * lxc - lbeta);
+    double tail;   // P(T <= -|t|) = I_x(a, b) / 2
+    if (x < (a + 1.0) / (a + b + 2.0)) tail = 0.5 * front * dev_betacf(a, b, x) / a;
+    else tail = 0.5 * (1.0 - front * dev_betacf(b, a, xc) / b);
+    if (!(xc > 0.0)) tail = 0.5;
+    return (t >= 0.0) ? 1.0 - tail : tail;
+}
+
+// log of the univariate t density t_1(0; loc, s2, m) given lgc = lgamma((m+1)/2) - lgamma(m/2).
+__device__ __forceinline__ double dev_t1_logpdf0(double loc, double s2, double m, double lgc) {
+    return lgc - 0.5 * log(m * CUDART_PI * s2) - 0.5 * (m + 1.0) * log1p(loc * loc / (m * s2));
+}
+
+// Regularized incomplete gamma: series for P (x < a + 1), Legendre CF for Q otherwise.
+__device__ inline double dev_gamma_series_P(double a, double x) {
+    double sum = 1.0 / a, term = sum, ap = a;
+    for (int k = 0; k < 10000; ++k) {
+        ap += 1.0;
+        term *= x / ap;
+        sum += term;
+        if (fabs(term) <= fabs(sum) * 1e-17) break;
+    }
+    return sum * exp(a * log(x) - x - lgamma(a));
+}
+__device__ inline double dev_gamma_cf_Q(double a, double x) {
+    const double fpmin = 1e-300;
+    double b = x + 1.0 - a, c = 1.0 / fpmin, d = 1.0 / b, h = d;
+    for (int k = 1; k < 10000; ++k) {
+        const double an = -k * (k - a);
+        b += 2.0;
+        d = an * d + b; d = (fabs(d) < fpmin) ? fpmin : d;
+        c = b + an / c; c = (fabs(c) < fpmin) ? fpmin : c;
+        d = 1.0 / d;
+        const double del = d * c;
+        h *= del;
+        if (fabs(del - 1.0) <= 1e-16) break;
+    }
+    return exp(a * log(x) - x - lgamma(a)) * h;
+}
+// log P(a,x) (upper = 0) or log Q(a,x) (upper = 1)
+__device__ inline double dev_log_gamma_PQ(double a, double x, int upper) {
+    if (x < a + 1.0) {
+        const double P = dev_gamma_series_P(a, x);
+        return upper ? log1p(-P) : log(P);
+    }
+    const double Q = dev_gamma_cf_Q(a, x);
+    return upper ? log(Q) : log1p(-Q);
+}
+
+// Chi-square quantile for real df m: solve P(m/2, v/2) = w (w <= 1/2) or Q(m/2, v/2) = 1 - w.
+// Newton on log F in s = log(v/2), bracketed; Wilson-Hilferty start.
+__device__ inline double dev_chi2_quantile(double w, double m) {
+    const double a = 0.5 * m;
+    const int upper = (w > 0.5);
+    const double ltarget = log(upper ? (1.0 - w) : w);
+    const double zq = Phiinv(w);
+    const double h9 = 2.0 / (9.0 * m);
+    double v = m * pow(fmax(1.0 - h9 + zq * sqrt(h9), 1e-3), 3.0);
+    double s = log(0.5 * v);
+    // small-v regime: P ~ x^a / Gamma(a+1)
+    const double s_small = (log(w) + lgamma(a + 1.0)) / a;
+    if (!upper && s_small < s) s = s_small;
+    double lo = -745.0, hi = fmax(0.0, log(a)) + 1.0;
+    for (int k = 0; k < 100; ++k) {   // make sure hi brackets from above
+        const double g = dev_log_gamma_PQ(a, exp(hi), upper) - ltarget;
+        if (upper ? (g < 0.0) : (g > 0.0)) break;
+        hi += 1.0;
+    }
+    if (!(s > lo && s < hi)) s = 0.5 * (lo + hi);
+    for (int it = 0; it < 300; ++it) {
+        const double x = exp(s);
+        const double lF = dev_log_gamma_PQ(a, x, upper);
+        const double g = lF - ltarget;
+        if (g == 0.0) break;
+        const bool root_below = upper ? (g < 0.0) : (g > 0.0);
+        if (root_below) hi = s; else lo = s;
+        // d log F / ds = x f(x) / F, f the Gamma(a,1) density; negative for Q
+        const double ldens = a * log(x) - x - lgamma(a);
+        double dg = exp(ldens - lF);
+        if (upper) dg = -dg;
+        double sn = s - g / dg;
+        if (fabs(sn - s) <= 1e-12 * fmax(1.0, fabs(s))) { s = sn; break; }
+        if (!(sn > lo && sn < hi)) sn = 0.5 * (lo + hi);
+        s = sn;
+    }
+    return 2.0 * exp(s);
+}
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+}  // namespace cfust

@@ -1,0 +1,957 @@
+// cfust_kernels.cu — FP64 CUDA kernels of the FM-CFUST EM hot path for sm_100a.
+//
+//   estep_cfust_kernel<Q,MODE>  q >= 1: one warp per observation j, looping over the g
+//                               components; the M lattice points of every T_r are split
+//                               over the 32 lanes and combined by xor-shuffle reductions
+//                               (Alg. 2; formulas DESIGN.md §3).
+//   estep_t_kernel              q == 0 (Delta = 0): one thread per
+//                               (observation, component), tiles of 32 observations.
+//   reduce_kernel               deterministic second pass over per-block partial sums.
+//   mstep_kernel                per-component M-step (Alg. 3; reading R-M).
+//   derive_kernel               Omega, chol, A, Lambda, constants.
+//   chi_kernel                  chi radius nodes of the lattice for df m0, m0+1, m0+2.
+//
+// No tensor cores: p, q <= 8 and the work is scalar special-function integration, not a
+// dense contraction (BASELINE.json north_star).
+#include "cfust_device.cuh"
+#include "cfust_internal.h"
+
+#include <cstdio>
+
+namespace cfust {
+
+constexpr int EW = 8;            // warps per block of the CFUST E-step
+constexpr int RW = 3 + QMAX + QMAX * QMAX;   // per-component result row in scratch
+
+// Per-warp scratch for the per-pair setup (written redundantly by all lanes with identical
+// values; every lane computes the same setup — SIMT issues it once per warp).
+struct WarpScratch {
+    double y[PMAX];
+    double c[QMAX];
+    double b[QMAX];
+    double Sp[QMAX * QMAX];
+    double ct[QMAX][QMAX];
+    double St[QMAX][QMAX * QMAX];
+    double Tk[QMAX];
+    double Tkt[QMAX * QMAX];
+    double phi[QMAX];
+    double bc[QMAX];
+    double Sc[QMAX * QMAX];
+    double res[GMAX][RW];        // [logf (no prior), e1me2, e2, e3[q], e4[q*q]]
+    double ll;
+};
+
+// ------------------------------------------------------------------------------------------
+// SOV point loop for T_R (chi-normal form, reading R-T): this lane's share of
+//   sum_l prod_k Phi(a_k(l)),  a_0 = s_l binv_0,  a_k = s_l binv_k - sum_{t<k} Cn_kt z_t,
+//   z_t = Phi^{-1}(clamp(w_{l,t+1} e_t)).
+template <int R>
+__device__ __forceinline__ double sov_lane_sum(const double (&binv)[R], const double (&Cn)[R * (R - 1) / 2],
+                                               const double *__restrict__ chi, const LatticeDev &L, int lane) {
+    double acc = 0.0;
+    for (int l = lane; l < L.M; l += 32) {
+        const double s = __ldg(chi + l);
+        double e = Phi(s * binv[0]);
+        double f = e;
+        double z[R - 1];
+#pragma unroll
+        for (int k = 1; k < R; ++k) {
+            const double w = lattice_w(L, l, k);
+            const double u = fmin(fmax(w * e, UMIN), UMAX);
+            z[k - 1] = Phiinv(u);
+            double a = s * binv[k];
+#pragma unroll
+            for (int t = 0; t < k; ++t) a -= Cn[(k * (k - 1)) / 2 + t] * z[t];
+            e = Phi(a);
+            f *= e;
+        }
+        acc += f;
+    }
+    return acc;
+}
+
+// T_R(b; 0, S, m): R = 0 -> 1; R = 1 -> univariate t CDF; R >= 2 -> lattice rule with
+// univariate-prioritisation reordering (ascending b_k / sqrt(S_kk), stable; reading A13).
+template <int R>
+__device__ double T_eval(const double *b, const double *S, int lds, double m, const double *__restrict__ chi,
+                         const LatticeDev &L, int lane) {
+    if constexpr (R == 0) {
+        return 1.0;
+    } else if constexpr (R == 1) {
+        return dev_t_cdf(b[0] / sqrt(S[0]), m);
+    } else {
+        int perm[R];
+        double key[R];
+#pragma unroll
+        for (int k = 0; k < R; ++k) { perm[k] = k; key[k] = b[k] / sqrt(S[k * lds + k]); }
+        for (int i = 1; i < R; ++i) {
+            const int pi = perm[i];
+            int j = i - 1;
+            while (j >= 0 && key[perm[j]] > key[pi]) { perm[j + 1] = perm[j]; --j; }
+            perm[j + 1] = pi;
+        }
+        double C[R][R];
+        for (int i = 0; i < R; ++i)
+            for (int j = 0; j <= i; ++j) {
+                double s = S[perm[i] * lds + perm[j]];
+                for (int k = 0; k < j; ++k) s -= C[i][k] * C[j][k];
+                if (i == j) {
+                    if (!(s > 1e-300)) return CUDART_NAN;
+                    C[i][i] = sqrt(s);
+                } else {
+                    C[i][j] = s / C[j][j];
+                }
+            }
+        double binv[R], Cn[R * (R - 1) / 2];
+#pragma unroll
+        for (int k = 0; k < R; ++k) binv[k] = b[perm[k]] / C[k][k];
+#pragma unroll
+        for (int k = 1; k < R; ++k)
+#pragma unroll
+            for (int t = 0; t < k; ++t) Cn[(k * (k - 1)) / 2 + t] = C[k][t] / C[k][k];
+        const double acc = sov_lane_sum<R>(binv, Cn, chi, L, lane);
+        return warp_sum(acc) / double(L.M);
+    }
+}
+
+// Per pair (observation in ws.y, component cp): O2-O8 of DESIGN.md §3.
+// MODE 1 computes only log f (T0).  Results go to res[] (identical in all lanes).
+template <int Q, int MODE>
+__device__ void pair_eval(const CompDev &cp, int p, const LatticeDev &L, const double *__restrict__ chi,
+                          WarpScratch &ws, double *res, int lane) {
+    double r[PMAX], v[PMAX];
+    double d = 0.0;
+#pragma unroll
+    for (int a = 0; a < PMAX; ++a) {
+        if (a < p) {
+            r[a] = ws.y[a] - cp.mu[a];
+            double s = r[a];
+#pragma unroll
+            for (int bb = 0; bb < a; ++bb) s -= cp.L[a * PMAX + bb] * v[bb];
+            v[a] = s * cp.Linv[a];
+            d += v[a] * v[a];
+        }
+    }
+    const double nu = cp.nu, m0 = cp.m0, rho = nu + d;
+    const double logt = cp.kappa - 0.5 * m0 * log1p(d / nu);
+    double c[Q];
+#pragma unroll
+    for (int k = 0; k < Q; ++k) {
+        double s = 0.0;
+#pragma unroll
+        for (int a = 0; a < PMAX; ++a)
+            if (a < p) s += cp.A[k * PMAX + a] * r[a];
+        c[k] = s;
+    }
+    const int M = L.M;
+    // T0 (density, Eq. (2)) and T2 (for e2)
+    const double sq0 = sqrt(m0 / rho);
+#pragma unroll
+    for (int k = 0; k < Q; ++k) ws.b[k] = c[k] * sq0;
+    const double T0 = T_eval<Q>(ws.b, cp.Lam, QMAX, m0, chi, L, lane);
+    if (MODE == 1) {
+        res[0] = (T0 > 0.0) ? Q * CUDART_LN2 + logt + log(T0) : -CUDART_INF;
+        return;
+    }
+    const double sq2 = sqrt((m0 + 2.0) / rho);
+#pragma unroll
+    for (int k = 0; k < Q; ++k) ws.b[k] = c[k] * sq2;
+    const double T2 = T_eval<Q>(ws.b, cp.Lam, QMAX, m0 + 2.0, chi + 2 * M, L, lane);
+    res[1] = cp.psi_half_m0 - log(0.5 * rho) - m0 / rho;      // e1 - e2, reading A5
+    if (!(T0 > 0.0)) {                                          // reading A16
+        res[0] = -CUDART_INF;
+        for (int k = 2; k < 3 + Q + Q * Q; ++k) res[k] = 0.0;
+        return;
+    }
+    // S' = (rho/m0) Lambda
+    const double sc = rho / m0;
+#pragma unroll
+    for (int k = 0; k < Q; ++k)
+#pragma unroll
+        for (int l = 0; l < Q; ++l) ws.Sp[k * QMAX + l] = sc * cp.Lam[k * QMAX + l];
+    const double *Sp = ws.Sp;
+    // phi_k = t_1(0; c_k, S'_kk, m0) and conditionals on x_k = 0 (df m0 + 1)
+    constexpr int Q1 = Q - 1;
+    constexpr int Q2 = (Q >= 2) ? Q - 2 : 0;
+    for (int k = 0; k < Q; ++k) {
+        const double skk = Sp[k * QMAX + k];
+        ws.phi[k] = exp(dev_t1_logpdf0(c[k], skk, m0, cp.lgc_m0));
+        if constexpr (Q >= 2) {
+            const double fac = (m0 + c[k] * c[k] / skk) / (m0 + 1.0);
+            int ia = 0;
+            for (int i = 0; i < Q; ++i) {
+                if (i == k) continue;
+                ws.ct[k][ia] = c[i] - Sp[i * QMAX + k] * c[k] / skk;
+                int ib = 0;
+                for (int j = 0; j < Q; ++j) {
+                    if (j == k) continue;
+                    ws.St[k][ia * QMAX + ib] = fac * (Sp[i * QMAX + j] - Sp[i * QMAX + k] * Sp[k * QMAX + j] / skk);
+                    ++ib;
+                }
+                ++ia;
+            }
+        }
+    }
+    const double rat = (m0 + 1.0) / (m0 - 1.0);   // S~' = rat * S~ (df m0 - 1)
+    // T_{q-2} for each pair {k < t}: condition t_{q-1}(c~(k), S~'(k), m0-1) on x_t = 0 (df m0)
+    if constexpr (Q >= 3) {
+        for (int k = 0; k < Q; ++k)
+            for (int t = k + 1; t < Q; ++t) {
+                const int at = t - 1;                  // position of t among "others of k" (t > k)
+                const double saa = rat * ws.St[k][at * QMAX + at];
+                const double cta = ws.ct[k][at];
+                const double fac2 = (m0 - 1.0 + cta * cta / saa) / m0;
+                int ib = 0;
+                for (int i = 0; i < Q1; ++i) {
+                    if (i == at) continue;
+                    const double sia = rat * ws.St[k][i * QMAX + at];
+                    ws.bc[ib] = ws.ct[k][i] - sia * cta / saa;
+                    int jb = 0;
+                    for (int j = 0; j < Q1; ++j) {
+                        if (j == at) continue;
+                        const double sij = rat * ws.St[k][i * QMAX + j];
+                        const double saj = rat * ws.St[k][at * QMAX + j];
+                        ws.Sc[ib * QMAX + jb] = fac2 * (sij - sia * saj / saa);
+                        ++jb;
+                    }
+                    ++ib;
+                }
+                const double val = T_eval<Q2>(ws.bc, ws.Sc, QMAX, m0, chi, L, lane);
+                ws.Tkt[k * QMAX + t] = val;
+                ws.Tkt[t * QMAX + k] = val;            // symmetric in {k, t} (A17)
+            }
+    }
+    // T_{q-1}(c~(k); 0, S~(k), m0+1) and h_k = phi_k T~(k)
+    double h[Q];
+#pragma unroll
+    for (int k = 0; k < Q; ++k) {
+        double tk = 1.0;
+        if constexpr (Q >= 2) tk = T_eval<Q1>(ws.ct[k], ws.St[k], QMAX, m0 + 1.0, chi + M, L, lane);
+        ws.Tk[k] = tk;
+        h[k] = ws.phi[k] * tk;
+    }
+    // E1 = c T2 + S' h
+    double E1[Q];
+#pragma unroll
+    for (int a = 0; a < Q; ++a) {
+        double s = c[a] * T2;
+#pragma unroll
+        for (int k = 0; k < Q; ++k) s += Sp[a * QMAX + k] * h[k];
+        E1[a] = s;
+    }
+    // G_kl = phi_k [ c~(k)_l T~(k) + (S~'(k) h(k))_l ],  h(k)_t = t_1(0; c~_t, S~'_tt, m0-1) T(k,t)
+    double G[Q][Q];
+#pragma unroll
+    for (int k = 0; k < Q; ++k)
+#pragma unroll
+        for (int l = 0; l < Q; ++l) G[k][l] = 0.0;
+    if constexpr (Q >= 2) {
+        for (int k = 0; k < Q; ++k) {
+            double hk[QMAX];
+            for (int a = 0; a < Q1; ++a) {
+                const int t = (a < k) ? a : a + 1;
+                const double saa = rat * ws.St[k][a * QMAX + a];
+                const double tkt = (Q >= 3) ? ws.Tkt[k * QMAX + t] : 1.0;
+                hk[a] = exp(dev_t1_logpdf0(ws.ct[k][a], saa, m0 - 1.0, cp.lgc_m0m1)) * tkt;
+            }
+            for (int a = 0; a < Q1; ++a) {
+                const int l = (a < k) ? a : a + 1;
+                double s = ws.ct[k][a] * ws.Tk[k];
+                for (int bb = 0; bb < Q1; ++bb) s += rat * ws.St[k][a * QMAX + bb] * hk[bb];
+                G[k][l] = ws.phi[k] * s;
+            }
+        }
+    }
+    // E2 = sym( S'(G + T0 I) + c E1' );  e2, e3, e4 (O8)
+    const double fr = m0 / rho;
+    const double inv = 1.0 / T0;
+    res[0] = Q * CUDART_LN2 + logt + log(T0);
+    res[2] = fr * T2 * inv;
+#pragma unroll
+    for (int a = 0; a < Q; ++a) res[3 + a] = fr * E1[a] * inv;
+    double E2[Q][Q];
+#pragma unroll
+    for (int a = 0; a < Q; ++a)
+#pragma unroll
+        for (int bb = 0; bb < Q; ++bb) {
+            double s = 0.0;
+#pragma unroll
+            for (int k = 0; k < Q; ++k) s += Sp[a * QMAX + k] * (G[k][bb] + (k == bb ? T0 : 0.0));
+            E2[a][bb] = s + c[a] * E1[bb];
+        }
+#pragma unroll
+    for (int a = 0; a < Q; ++a)
+#pragma unroll
+        for (int bb = 0; bb < Q; ++bb) res[3 + Q + a * Q + bb] = fr * 0.5 * (E2[a][bb] + E2[bb][a]) * inv;
+}
+
+// Stats entry decode: code = type | i << 4 | a << 8 | b << 12
+enum : int { ST_S0 = 0, ST_S1, ST_S2, ST_S3, ST_S4, ST_S5, ST_S6, ST_S7 };
+
+__device__ inline int stat_code(int e, int p, int q, int K) {
+    const int i = e / K;
+    int k = e % K;
+    int type, a = 0, b = 0;
+    if (k == 0) type = ST_S0;
+    else if (k == 1) type = ST_S1;
+    else if ((k -= 2) < p) { type = ST_S2; a = k; }
+    else if ((k -= p) < p * (p + 1) / 2) {
+        type = ST_S3;
+        int row = 0;
+        while (k >= p - row) { k -= p - row; ++row; }
+        a = row; b = row + k;
+    } else if ((k -= p * (p + 1) / 2) < q) { type = ST_S4; a = k; }
+    else if ((k -= q) < q * (q + 1) / 2) {
+        type = ST_S5;
+        int row = 0;
+        while (k >= q - row) { k -= q - row; ++row; }
+        a = row; b = row + k;
+    } else if ((k -= q * (q + 1) / 2) < p * q) { type = ST_S6; a = k / q; b = k % q; }
+    else type = ST_S7;
+    return type | (i << 4) | (a << 8) | (b << 12);
+}
+
+struct EArgs {
+    const double *__restrict__ y;
+    int64_t n;
+    int p, g, K;
+    const CompDev *__restrict__ comp;
+    const double *__restrict__ chi;
+    LatticeDev lat;
+    double *__restrict__ partials;
+    int *status;
+    const int64_t *__restrict__ idx;
+    int64_t cnt;
+    double *__restrict__ pair_out;
+};
+
+// MODE 0: E-step statistics; 1: log-likelihood only; 2: per-pair dump of idx[0..cnt).
+template <int Q, int MODE>
+__global__ void __launch_bounds__(EW * 32) estep_cfust_kernel(EArgs A) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int p = A.p, g = A.g, K = A.K, GK = g * K;
+    CompDev *comp = reinterpret_cast<CompDev *>(smem_raw);
+    WarpScratch *wsa = reinterpret_cast<WarpScratch *>(comp + g);
+    double *acc_all = reinterpret_cast<double *>(wsa + EW);          // [EW][GK + 1]
+    int *codes = reinterpret_cast<int *>(acc_all + EW * (GK + 1));   // [GK]
+    for (int t = threadIdx.x; t < g * int(sizeof(CompDev) / sizeof(double)); t += blockDim.x)
+        reinterpret_cast<double *>(comp)[t] = reinterpret_cast<const double *>(A.comp)[t];
+    for (int e = threadIdx.x; e < GK; e += blockDim.x) codes[e] = stat_code(e, p, Q, K);
+    for (int e = threadIdx.x; e < EW * (GK + 1); e += blockDim.x) acc_all[e] = 0.0;
+    __syncthreads();
+    WarpScratch &ws = wsa[wid];
+    double *acc = acc_all + wid * (GK + 1);
+    const int M = A.lat.M;
+    const int64_t nwarps = int64_t(gridDim.x) * EW;
+    const int64_t total = (MODE == 2) ? A.cnt : A.n;
+    double ll = 0.0;
+    for (int64_t jj = int64_t(blockIdx.x) * EW + wid; jj < total; jj += nwarps) {
+        const int64_t j = (MODE == 2) ? A.idx[jj] : jj;
+        __syncwarp();
+        if (lane < p) ws.y[lane] = A.y[j * p + lane];
+        __syncwarp();
+        for (int i = 0; i < g; ++i)
+            pair_eval<Q, MODE == 1 ? 1 : 0>(comp[i], p, A.lat, A.chi + size_t(i) * 3 * M, ws, ws.res[i], lane);
+        __syncwarp();
+        // Eq. (3)-(4): LSE over components, tau
+        double lf[GMAX], mx = -CUDART_INF;
+#pragma unroll
+        for (int i = 0; i < GMAX; ++i)
+            if (i < g) { lf[i] = comp[i].logpi + ws.res[i][0]; mx = fmax(mx, lf[i]); }
+        if (mx == -CUDART_INF) {
+            if (lane == 0) atomicOr(A.status, 1);
+            continue;
+        }
+        double se = 0.0;
+#pragma unroll
+        for (int i = 0; i < GMAX; ++i)
+            if (i < g) se += exp(lf[i] - mx);
+        const double lse = mx + log(se);
+        ll += lse;
+        if constexpr (MODE == 1) continue;
+        double tau[GMAX];
+#pragma unroll
+        for (int i = 0; i < GMAX; ++i) tau[i] = (i < g) ? exp(lf[i] - lse) : 0.0;
+        if constexpr (MODE == 2) {
+            const int PWo = 4 + Q + Q * Q;
+            double *o = A.pair_out + size_t(jj) * g * PWo;
+            for (int e = lane; e < g * PWo; e += 32) {
+                const int i = e / PWo, k = e % PWo;
+                double lfi = 0.0, ti = 0.0;
+#pragma unroll
+                for (int c2 = 0; c2 < GMAX; ++c2)
+                    if (c2 == i) { lfi = lf[c2]; ti = tau[c2]; }
+                o[e] = (k == 0) ? lfi : (k == 1) ? ti : ws.res[i][k - 1];
+            }
+            continue;
+        }
+        // accumulate the eight sufficient statistics (reading A4); lane-owned entries
+        for (int e = lane; e < GK; e += 32) {
+            const int code = codes[e];
+            const int type = code & 15, i = (code >> 4) & 15, a = (code >> 8) & 15, bq = (code >> 12) & 15;
+            double ti = 0.0;
+#pragma unroll
+            for (int c2 = 0; c2 < GMAX; ++c2)
+                if (c2 == i) ti = tau[c2];
+            if (!(ti > 0.0)) continue;
+            const double *rs = ws.res[i];
+            double val;
+            switch (type) {
+                case ST_S0: val = 1.0; break;
+                case ST_S1: val = rs[2]; break;
+                case ST_S2: val = rs[2] * ws.y[a]; break;
+                case ST_S3: val = rs[2] * ws.y[a] * ws.y[bq]; break;
+                case ST_S4: val = rs[3 + a]; break;
+                case ST_S5: val = rs[3 + Q + a * Q + bq]; break;
+                case ST_S6: val = ws.y[a] * rs[3 + bq]; break;
+                default: val = rs[1]; break;
+            }
+            acc[e] += ti * val;
+        }
+    }
+    if (MODE == 2) return;
+    if (lane == 0) acc[GK] = ll;
+    __syncthreads();
+    double *out = A.partials + size_t(blockIdx.x) * (GK + 1);
+    for (int e = threadIdx.x; e <= GK; e += blockDim.x) {
+        double s = 0.0;
+        for (int w = 0; w < EW; ++w) s += acc_all[w * (GK + 1) + e];
+        out[e] = s;
+    }
+}
+
+// ------------------------------------------------------------------------------------------
+// q == 0: t-mixture E-step (Delta = 0).  Block = g warps x TW tiles; warp
+// (i, tile) evaluates component i for 32 observations (one per lane) and keeps its 3+p+
+// p(p+1)/2 statistics in registers; tau needs all g log-densities -> exchanged via smem.
+constexpr int TW = 1;   // observation tiles (of 32) per block
+
+template <int P>
+__global__ void __launch_bounds__(GMAX * TW * 32) estep_t_kernel(EArgs A, int mode) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int g = A.g, K = A.K, GK = g * K;
+    const int comp_i = wid % g, tile = wid / g;
+    const bool active_warp = wid < g * TW;
+    CompDev *comp = reinterpret_cast<CompDev *>(smem_raw);
+    double *ys = reinterpret_cast<double *>(comp + g);                  // [TW*32][P+1]
+    double *lfs = ys + TW * 32 * (P + 1);                                // [TW][GMAX][32]
+    double *lse_s = lfs + TW * GMAX * 32;                                // [TW][32]
+    double *red = lse_s + TW * 32;                                       // [g*TW][K+1] block reduce
+    for (int t = threadIdx.x; t < g * int(sizeof(CompDev) / sizeof(double)); t += blockDim.x)
+        reinterpret_cast<double *>(comp)[t] = reinterpret_cast<const double *>(A.comp)[t];
+    __syncthreads();
+    const CompDev &cp = comp[comp_i];
+    constexpr int NS = 3 + P + P * (P + 1) / 2;   // S0, S1, S2[P], S3[P(P+1)/2], S7
+    double st[NS];
+#pragma unroll
+    for (int k = 0; k < NS; ++k) st[k] = 0.0;
+    double ll = 0.0;
+    const int64_t n = A.n;
+    const int64_t ntiles = (n + 32 * TW - 1) / (32 * TW);
+    for (int64_t tb = blockIdx.x; tb < ntiles; tb += gridDim.x) {
+        const int64_t j0 = tb * 32 * TW;
+        const int64_t rows = (n - j0 < 32 * TW) ? (n - j0) : int64_t(32 * TW);
+        __syncthreads();
+        for (int t = threadIdx.x; t < rows * P; t += blockDim.x) {
+            const int rr = t / P, a = t % P;
+            ys[rr * (P + 1) + a] = A.y[j0 * P + t];
+        }
+        __syncthreads();
+        const int row = tile * 32 + lane;
+        const bool valid = active_warp && row < rows;
+        double y[P], dd = 0.0, lf = -CUDART_INF;
+        if (valid) {
+            double v[P];
+#pragma unroll
+            for (int a = 0; a < P; ++a) y[a] = ys[row * (P + 1) + a];
+#pragma unroll
+            for (int a = 0; a < P; ++a) {
+                double s = y[a] - cp.mu[a];
+#pragma unroll
+                for (int bb = 0; bb < a; ++bb) s -= cp.L[a * PMAX + bb] * v[bb];
+                v[a] = s * cp.Linv[a];
+                dd += v[a] * v[a];
+            }
+            lf = cp.logpi + cp.kappa - 0.5 * cp.m0 * log1p(dd / cp.nu);
+            lfs[(tile * GMAX + comp_i) * 32 + lane] = lf;
+        }
+        __syncthreads();
+        if (valid && comp_i == 0) {   // LSE over components for this observation
+            double mx = -CUDART_INF;
+            for (int i = 0; i < g; ++i) mx = fmax(mx, lfs[(tile * GMAX + i) * 32 + lane]);
+            double se = 0.0;
+            for (int i = 0; i < g; ++i) se += exp(lfs[(tile * GMAX + i) * 32 + lane] - mx);
+            const double lse = (mx == -CUDART_INF) ? mx : mx + log(se);
+            if (mx == -CUDART_INF) atomicOr(A.status, 1);
+            lse_s[tile * 32 + lane] = lse;
+            ll += lse;
+        }
+        __syncthreads();
+        if (valid && mode == 0) {
+            const double lse = lse_s[tile * 32 + lane];
+            const double tau = exp(lf - lse);
+            if (tau > 0.0) {
+                const double rho = cp.nu + dd;
+                const double e2 = cp.m0 / rho;
+                const double e1me2 = cp.psi_half_m0 - log(0.5 * rho) - e2;
+                const double te2 = tau * e2;
+                st[0] += tau;
+                st[1] += te2;
+                int o = 2;
+#pragma unroll
+                for (int a = 0; a < P; ++a) st[o + a] += te2 * y[a];
+                o += P;
+#pragma unroll
+                for (int a = 0; a < P; ++a) {
+                    const double ta = te2 * y[a];
+#pragma unroll
+                    for (int bb = a; bb < P; ++bb) st[o++] += ta * y[bb];
+                }
+                st[NS - 1] += tau * e1me2;
+            }
+        }
+    }
+    // block reduction: lanes -> warp (shuffle tree), warps (i, tile) -> block (fixed order)
+#pragma unroll
+    for (int k = 0; k < NS; ++k) st[k] = warp_sum(st[k]);
+    ll = warp_sum(ll);
+    __syncthreads();
+    if (active_warp && lane == 0) {
+        double *r = red + size_t(wid) * (K + 1);
+#pragma unroll
+        for (int k = 0; k < NS; ++k) r[k] = st[k];
+        r[K] = (comp_i == 0) ? ll : 0.0;
+    }
+    __syncthreads();
+    if (mode == 1) {
+        if (threadIdx.x == 0) {
+            double s = 0.0;
+            for (int t = 0; t < TW; ++t) s += red[size_t(t * g) * (K + 1) + K];
+            A.partials[size_t(blockIdx.x) * (GK + 1) + GK] = s;
+        }
+        return;
+    }
+    double *out = A.partials + size_t(blockIdx.x) * (GK + 1);
+    for (int e = threadIdx.x; e <= GK; e += blockDim.x) {
+        double s = 0.0;
+        if (e < GK) {
+            const int i = e / K, k = e % K;
+            for (int t = 0; t < TW; ++t) s += red[size_t(t * g + i) * (K + 1) + k];
+        } else {
+            for (int t = 0; t < TW; ++t) s += red[size_t(t * g) * (K + 1) + K];
+        }
+        out[e] = s;
+    }
+}
+
+// ------------------------------------------------------------------------------------------
+__global__ void reduce_kernel(const double *__restrict__ partials, int nblocks, int stride, int col0, int ncols,
+                              double *__restrict__ out) {
+    for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < ncols; e += gridDim.x * blockDim.x) {
+        double s = 0.0;
+        for (int b = 0; b < nblocks; ++b) s += partials[size_t(b) * stride + col0 + e];   // ascending block order
+        out[e] = s;
+    }
+}
+
+// q == 0 per-pair dump for parity checks: one thread per listed observation.
+__global__ void dump_t_kernel(EArgs A) {
+    const int g = A.g, p = A.p;
+    for (int64_t jj = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; jj < A.cnt; jj += int64_t(gridDim.x) * blockDim.x) {
+        const int64_t j = A.idx[jj];
+        double lf[GMAX], e2[GMAX], e1me2[GMAX], mx = -CUDART_INF;
+        for (int i = 0; i < g; ++i) {
+            const CompDev &cp = A.comp[i];
+            double v[PMAX], dd = 0.0;
+            for (int a = 0; a < p; ++a) {
+                double s = A.y[j * p + a] - cp.mu[a];
+                for (int bb = 0; bb < a; ++bb) s -= cp.L[a * PMAX + bb] * v[bb];
+                v[a] = s * cp.Linv[a];
+                dd += v[a] * v[a];
+            }
+            const double rho = cp.nu + dd;
+            lf[i] = cp.logpi + cp.kappa - 0.5 * cp.m0 * log1p(dd / cp.nu);
+            e2[i] = cp.m0 / rho;
+            e1me2[i] = cp.psi_half_m0 - log(0.5 * rho) - e2[i];
+            mx = fmax(mx, lf[i]);
+        }
+        double se = 0.0;
+        for (int i = 0; i < g; ++i) se += exp(lf[i] - mx);
+        const double lse = mx + log(se);
+        double *o = A.pair_out + size_t(jj) * g * 4;
+        for (int i = 0; i < g; ++i) {
+            o[i * 4 + 0] = lf[i];
+            o[i * 4 + 1] = exp(lf[i] - lse);
+            o[i * 4 + 2] = e1me2[i];
+            o[i * 4 + 3] = e2[i];
+        }
+    }
+}
+
+// ------------------------------------------------------------------------------------------
+// Small dense helpers (single thread).
+__device__ inline bool chol_dev(int n, const double *S, int lds, double *L, int ldl) {
+    for (int i = 0; i < n; ++i)
+        for (int j = 0; j <= i; ++j) {
+            double s = S[i * lds + j];
+            for (int k = 0; k < j; ++k) s -= L[i * ldl + k] * L[j * ldl + k];
+            if (i == j) {
+                if (!(s > 1e-300)) return false;
+                L[i * ldl + i] = sqrt(s);
+            } else {
+                L[i * ldl + j] = s / L[j * ldl + j];
+            }
+        }
+    return true;
+}
+__device__ inline void chol_solve_dev(int n, const double *L, int ldl, double *x) {
+    for (int i = 0; i < n; ++i) {
+        double s = x[i];
+        for (int k = 0; k < i; ++k) s -= L[i * ldl + k] * x[k];
+        x[i] = s / L[i * ldl + i];
+    }
+    for (int i = n - 1; i >= 0; --i) {
+        double s = x[i];
+        for (int k = i + 1; k < n; ++k) s -= L[k * ldl + i] * x[k];
+        x[i] = s / L[i * ldl + i];
+    }
+}
+
+// Derived quantities for component i.
+__device__ int derive_one(const DevState &s, int i, CompDev &cd) {
+    const int p = s.p, q = s.q;
+    const double *Sg = s.sigma + size_t(i) * p * p;
+    const double *D = s.delta + size_t(i) * p * q;
+    double Om[PMAX * PMAX];
+    for (int a = 0; a < p; ++a)
+        for (int b = 0; b < p; ++b) {
+            double v = Sg[a * p + b];
+            for (int k = 0; k < q; ++k) v += D[a * q + k] * D[b * q + k];
+            Om[a * PMAX + b] = v;
+        }
+    for (int t = 0; t < PMAX * PMAX; ++t) cd.L[t] = 0.0;
+    if (!chol_dev(p, Om, PMAX, cd.L, PMAX)) return -4;
+    double logdet = 0.0;
+    for (int a = 0; a < p; ++a) { cd.Linv[a] = 1.0 / cd.L[a * PMAX + a]; logdet += 2.0 * log(cd.L[a * PMAX + a]); }
+    for (int a = p; a < PMAX; ++a) cd.Linv[a] = 0.0;
+    for (int a = 0; a < p; ++a) cd.mu[a] = s.mu[size_t(i) * p + a];
+    for (int t = 0; t < QMAX * PMAX; ++t) cd.A[t] = 0.0;
+    for (int t = 0; t < QMAX * QMAX; ++t) cd.Lam[t] = 0.0;
+    for (int k = 0; k < q; ++k) {
+        double x[PMAX];
+        for (int a = 0; a < p; ++a) x[a] = D[a * q + k];
+        chol_solve_dev(p, cd.L, PMAX, x);
+        for (int a = 0; a < p; ++a) cd.A[k * PMAX + a] = x[a];
+    }
+    for (int k = 0; k < q; ++k)
+        for (int l = 0; l < q; ++l) {
+            double v = 0.0;
+            for (int a = 0; a < p; ++a) v += D[a * q + k] * cd.A[l * PMAX + a];
+            cd.Lam[k * QMAX + l] = (k == l ? 1.0 : 0.0) - v;
+        }
+    for (int k = 0; k < q; ++k)
+        for (int l = k + 1; l < q; ++l) {
+            const double v = 0.5 * (cd.Lam[k * QMAX + l] + cd.Lam[l * QMAX + k]);
+            cd.Lam[k * QMAX + l] = v;
+            cd.Lam[l * QMAX + k] = v;
+        }
+    const double nu = s.nu[i], m0 = nu + p;
+    cd.nu = nu;
+    cd.m0 = m0;
+    cd.kappa = lgamma(0.5 * m0) - lgamma(0.5 * nu) - 0.5 * p * log(nu * CUDART_PI) - 0.5 * logdet;
+    cd.logpi = log(s.pi[i]);
+    cd.psi_half_m0 = dev_digamma(0.5 * m0);
+    cd.lgc_m0 = lgamma(0.5 * (m0 + 1.0)) - lgamma(0.5 * m0);
+    cd.lgc_m0m1 = lgamma(0.5 * m0) - lgamma(0.5 * (m0 - 1.0));
+    cd.pad = 0.0;
+    return 0;
+}
+
+__global__ void derive_kernel(DevState s) {
+    const int i = threadIdx.x;
+    if (i < s.g) {
+        const int rc = derive_one(s, i, s.comp[i]);
+        if (rc != 0) atomicMin(s.status + 1, rc);
+    }
+}
+
+__device__ inline double nu_equation(double nu, double c) { return log(0.5 * nu) - dev_digamma(0.5 * nu) + 1.0 + c; }
+
+// M-step for component i (ECM order, reading A6) from the global statistics.
+__device__ int mstep_one(const DevState &s, int i) {
+    const int p = s.p, q = s.q, K = s.K;
+    const double *S = s.stats + size_t(i) * K;
+    const double S0 = S[0], S1 = S[1];
+    const double *S2 = S + 2, *S3p = S2 + p, *S4 = S3p + p * (p + 1) / 2, *S5p = S4 + q;
+    const double *S6 = S5p + q * (q + 1) / 2;
+    const double S7 = S6[p * q];
+    if (!(S0 >= 1e-10)) return -6;
+    double S3[PMAX * PMAX], S5[QMAX * QMAX];
+    {
+        int o = 0;
+        for (int a = 0; a < p; ++a)
+            for (int b = a; b < p; ++b) { S3[a * PMAX + b] = S3p[o]; S3[b * PMAX + a] = S3p[o]; ++o; }
+        o = 0;
+        for (int k = 0; k < q; ++k)
+            for (int l = k; l < q; ++l) { S5[k * QMAX + l] = S5p[o]; S5[l * QMAX + k] = S5p[o]; ++o; }
+    }
+    double *mu = s.mu + size_t(i) * p, *Sg = s.sigma + size_t(i) * p * p, *D = s.delta + size_t(i) * p * q;
+    for (int a = 0; a < p; ++a) {
+        double v = S2[a];
+        for (int k = 0; k < q; ++k) v -= D[a * q + k] * S4[k];
+        mu[a] = v / S1;
+    }
+    double B[PMAX * QMAX];
+    for (int a = 0; a < p; ++a)
+        for (int k = 0; k < q; ++k) B[a * QMAX + k] = S6[a * q + k] - mu[a] * S4[k];
+    if (q > 0) {
+        double L5[QMAX * QMAX];
+        if (!chol_dev(q, S5, QMAX, L5, QMAX)) return -4;
+        for (int a = 0; a < p; ++a) {
+            double x[QMAX];
+            for (int k = 0; k < q; ++k) x[k] = B[a * QMAX + k];
+            chol_solve_dev(q, L5, QMAX, x);
+            for (int k = 0; k < q; ++k) D[a * q + k] = x[k];
+        }
+    }
+    for (int a = 0; a < p; ++a)
+        for (int b = 0; b < p; ++b) {
+            double v = S3[a * PMAX + b] - S2[a] * mu[b] - mu[a] * S2[b] + S1 * mu[a] * mu[b];
+            for (int k = 0; k < q; ++k) v -= B[a * QMAX + k] * D[b * q + k] + D[a * q + k] * B[b * QMAX + k];
+            for (int k = 0; k < q; ++k)
+                for (int l = 0; l < q; ++l) v += D[a * q + k] * S5[k * QMAX + l] * D[b * q + l];
+            Sg[a * p + b] = v / S0;
+        }
+    for (int a = 0; a < p; ++a)
+        for (int b = a + 1; b < p; ++b) {
+            const double v = 0.5 * (Sg[a * p + b] + Sg[b * p + a]);
+            Sg[a * p + b] = v;
+            Sg[b * p + a] = v;
+        }
+    double Lt[PMAX * PMAX];
+    if (!chol_dev(p, Sg, p, Lt, PMAX)) {   // ridge repair
+        double md = 0.0;
+        for (int a = 0; a < p; ++a) md += Sg[a * p + a];
+        md /= p;
+        for (int a = 0; a < p; ++a) Sg[a * p + a] += 1e-8 * md;
+        if (!chol_dev(p, Sg, p, Lt, PMAX)) return -4;
+    }
+    const double cst = S7 / S0;
+    double nu;
+    if (nu_equation(s.nu_hi, cst) > 0.0) nu = s.nu_hi;
+    else if (nu_equation(s.nu_lo, cst) < 0.0) nu = s.nu_lo;
+    else {
+        double lo = s.nu_lo, hi = s.nu_hi;
+        for (int it = 0; it < 400; ++it) {
+            const double mid = 0.5 * (lo + hi);
+            if (nu_equation(mid, cst) > 0.0) lo = mid; else hi = mid;
+            if (hi - lo <= 1e-12 * 0.5 * (lo + hi)) break;
+        }
+        nu = 0.5 * (lo + hi);
+    }
+    s.nu[i] = nu;
+    return 0;
+}
+
+__global__ void mstep_kernel(DevState s) {
+    const int i = threadIdx.x;
+    __shared__ int bad;
+    if (i == 0) bad = 0;
+    __syncthreads();
+    if (i < s.g) {
+        const int rc = mstep_one(s, i);
+        if (rc != 0) { atomicMin(s.status + 1, rc); bad = 1; }
+    }
+    __syncthreads();
+    if (i == 0 && !bad) {   // pi <- S0 / n_total, floored at 1e-10, renormalised
+        double tot = 0.0;
+        for (int c = 0; c < s.g; ++c) {
+            double v = s.stats[size_t(c) * s.K] / s.n_total;
+            v = (v < 1e-10) ? 1e-10 : v;
+            s.pi[c] = v;
+            tot += v;
+        }
+        for (int c = 0; c < s.g; ++c) s.pi[c] /= tot;
+    }
+    __syncthreads();
+    if (i < s.g && !bad) {
+        const int rc = derive_one(s, i, s.comp[i]);
+        if (rc != 0) atomicMin(s.status + 1, rc);
+    }
+}
+
+// chi radius nodes: chi[(i*3 + k)*M + l] = sqrt(chi2_{m0+k}^{-1}(w_{l,0}) / (m0+k))
+__global__ void chi_kernel(DevState s, LatticeDev L) {
+    const int total = s.g * 3 * L.M;
+    for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < total; t += gridDim.x * blockDim.x) {
+        const int l = t % L.M, ik = t / L.M, i = ik / 3, k = ik % 3;
+        const double m = s.comp[i].m0 + double(k);
+        const double w = lattice_w(L, l, 0);
+        s.chi[t] = sqrt(dev_chi2_quantile(w, m) / m);
+    }
+}
+
+__global__ void check_finite_kernel(const double *__restrict__ y, int64_t count, int *flag) {
+    for (int64_t t = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; t < count; t += int64_t(gridDim.x) * blockDim.x)
+        if (!isfinite(y[t])) atomicOr(flag, 1);
+}
+
+// ------------------------------------------------------------------------------------------
+// Launchers
+static LatticeDev make_lattice(const DevState &s) {
+    LatticeDev L;
+    L.M = s.M > 0 ? s.M : 32;
+    for (int k = 0; k < QMAX; ++k) { L.z[k] = s.z[k]; L.shift[k] = s.shift[k]; }
+    return L;
+}
+
+size_t comp_dev_size() { return sizeof(CompDev); }
+
+static size_t cfust_smem(const DevState &s) {
+    const int GK = s.g * s.K;
+    return sizeof(CompDev) * s.g + sizeof(WarpScratch) * EW + sizeof(double) * EW * (GK + 1) + sizeof(int) * GK;
+}
+
+static size_t t_smem(const DevState &s) {
+    const int P = s.p;
+    return sizeof(CompDev) * s.g + sizeof(double) * (TW * 32 * (P + 1) + TW * GMAX * 32 + TW * 32) +
+           sizeof(double) * size_t(s.g * TW) * (s.K + 1);
+}
+
+template <int Q, int MODE>
+static int launch_cfust_q(const DevState &s, EArgs &a, cudaStream_t st, int *nb) {
+    auto kern = estep_cfust_kernel<Q, MODE>;
+    const size_t sm = cfust_smem(s);
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
+    if (e != cudaSuccess) return int(e);
+    int per_sm = 0;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, EW * 32, sm);
+    if (e != cudaSuccess) return int(e);
+    if (per_sm < 1) per_sm = 1;
+    const int64_t work = (MODE == 2) ? a.cnt : a.n;
+    int64_t blocks = int64_t(s.num_sms) * per_sm;
+    const int64_t need = (work + EW - 1) / EW;
+    if (blocks > need) blocks = need;
+    if (blocks < 1) blocks = 1;
+    kern<<<int(blocks), EW * 32, sm, st>>>(a);
+    *nb = int(blocks);
+    return int(cudaGetLastError());
+}
+
+template <int MODE>
+static int launch_cfust_mode(const DevState &s, EArgs &a, cudaStream_t st, int *nb) {
+    switch (s.q) {
+        case 1: return launch_cfust_q<1, MODE>(s, a, st, nb);
+        case 2: return launch_cfust_q<2, MODE>(s, a, st, nb);
+        case 3: return launch_cfust_q<3, MODE>(s, a, st, nb);
+        case 4: return launch_cfust_q<4, MODE>(s, a, st, nb);
+        case 5: return launch_cfust_q<5, MODE>(s, a, st, nb);
+        case 6: return launch_cfust_q<6, MODE>(s, a, st, nb);
+        default: return int(cudaErrorInvalidValue);
+    }
+}
+
+template <int P>
+static int launch_t_p(const DevState &s, EArgs &a, int mode, cudaStream_t st, int *nb) {
+    auto kern = estep_t_kernel<P>;
+    const size_t sm = t_smem(s);
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
+    if (e != cudaSuccess) return int(e);
+    const int threads = s.g * TW * 32;
+    int per_sm = 0;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, sm);
+    if (e != cudaSuccess) return int(e);
+    if (per_sm < 1) per_sm = 1;
+    const int64_t ntiles = (a.n + 32 * TW - 1) / (32 * TW);
+    int64_t blocks = int64_t(s.num_sms) * per_sm;
+    if (blocks > ntiles) blocks = ntiles;
+    if (blocks < 1) blocks = 1;
+    kern<<<int(blocks), threads, sm, st>>>(a, mode);
+    *nb = int(blocks);
+    return int(cudaGetLastError());
+}
+
+int max_partial_blocks(const DevState &s) { return s.num_sms * 32; }
+
+int launch_estep(const DevState &s, int mode, const int64_t *idx, int64_t cnt, double *pair_out, cudaStream_t st,
+                 int *nblocks_out) {
+    EArgs a;
+    a.y = s.y;
+    a.n = s.n;
+    a.p = s.p;
+    a.g = s.g;
+    a.K = s.K;
+    a.comp = s.comp;
+    a.chi = s.chi;
+    a.lat = make_lattice(s);
+    a.partials = s.partials;
+    a.status = s.status;
+    a.idx = idx;
+    a.cnt = cnt;
+    a.pair_out = pair_out;
+    *nblocks_out = 0;
+    if (s.q == 0) {
+        if (mode == 2) {
+            int64_t blocks = (cnt + 127) / 128;
+            if (blocks < 1) blocks = 1;
+            dump_t_kernel<<<int(blocks > 4096 ? 4096 : blocks), 128, 0, st>>>(a);
+            return int(cudaGetLastError());
+        }
+        switch (s.p) {
+            case 1: return launch_t_p<1>(s, a, mode, st, nblocks_out);
+            case 2: return launch_t_p<2>(s, a, mode, st, nblocks_out);
+            case 3: return launch_t_p<3>(s, a, mode, st, nblocks_out);
+            case 4: return launch_t_p<4>(s, a, mode, st, nblocks_out);
+            case 5: return launch_t_p<5>(s, a, mode, st, nblocks_out);
+            case 6: return launch_t_p<6>(s, a, mode, st, nblocks_out);
+            case 7: return launch_t_p<7>(s, a, mode, st, nblocks_out);
+            case 8: return launch_t_p<8>(s, a, mode, st, nblocks_out);
+            default: return int(cudaErrorInvalidValue);
+        }
+    }
+    switch (mode) {
+        case 0: return launch_cfust_mode<0>(s, a, st, nblocks_out);
+        case 1: return launch_cfust_mode<1>(s, a, st, nblocks_out);
+        case 2: return launch_cfust_mode<2>(s, a, st, nblocks_out);
+        default: return int(cudaErrorInvalidValue);
+    }
+}
+
+int launch_reduce(const DevState &s, int nblocks, int mode, double *out, cudaStream_t st) {
+    const int len = s.g * s.K + 1;
+    if (mode == 1)   // log-likelihood only: column GK
+        reduce_kernel<<<1, 32, 0, st>>>(s.partials, nblocks, len, len - 1, 1, out);
+    else
+        reduce_kernel<<<(len + 127) / 128, 128, 0, st>>>(s.partials, nblocks, len, 0, len, out);
+    return int(cudaGetLastError());
+}
+
+int launch_mstep(const DevState &s, cudaStream_t st) {
+    mstep_kernel<<<1, 32, 0, st>>>(s);
+    return int(cudaGetLastError());
+}
+
+int launch_derive(const DevState &s, cudaStream_t st) {
+    derive_kernel<<<1, 32, 0, st>>>(s);
+    return int(cudaGetLastError());
+}
+
+int launch_chi(const DevState &s, cudaStream_t st) {
+    if (s.q < 2 || s.M <= 0) return 0;
+    const LatticeDev L = make_lattice(s);
+    const int total = s.g * 3 * s.M;
+    chi_kernel<<<(total + 127) / 128, 128, 0, st>>>(s, L);
+    return int(cudaGetLastError());
+}
+
+int launch_check_finite(const double *y, int64_t count, int *flag, cudaStream_t st) {
+    if (count <= 0) return 0;
+    int64_t blocks = (count + 255) / 256;
+    if (blocks > 4096) blocks = 4096;
+    check_finite_kernel<<<int(blocks), 256, 0, st>>>(y, count, flag);
+    return int(cudaGetLastError());
+}
+
+}  // namespace cfust
