@@ -37,9 +37,9 @@ UNIT = "(obs·component)/s"
 # the same box is reported beside it (fp64_peak_measured_tflops).
 FP64_PEAK_NOMINAL_TFLOPS = 148 * 64 * 2 * 1.965e9 / 1e12
 # Executed FP64 flops of the E-step kernel per (obs, component) pair at cfg2, from the ncu
-# counters 2*dfma + dadd + dmul (profiles/r01_ncu_estep_cfg2.txt).  None until
-# measured; bench then reports roofline from SOV-evaluation counts only.
-FP64_FLOPS_PER_PAIR = {2: None}
+# counters 2*dfma + dadd + dmul over one E-step launch at n=4000 (12000 pairs):
+# profiles/r01_ncu_estep_cfg2.txt.  Re-measured whenever the kernel changes.
+FP64_FLOPS_PER_PAIR = {2: 1.2090e7}
 
 
 def env_rank():

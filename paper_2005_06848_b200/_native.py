@@ -6,7 +6,7 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libcfust.so")
+LIB_PATH = os.environ.get("CFUST_LIB") or os.path.join(_HERE, "libcfust.so")   # CFUST_LIB: experiment builds
 
 CFUST_OK, CFUST_EINVAL, CFUST_EDIM, CFUST_EMIXPROP, CFUST_ENOTPD = 0, -1, -2, -3, -4
 CFUST_EUNDERFLOW, CFUST_EEMPTY, CFUST_ECUDA, CFUST_ENCCL = -5, -6, -7, -8

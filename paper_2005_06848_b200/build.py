@@ -10,7 +10,7 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libcfust.so")
 SOURCES = ["cfust_kernels.cu", "cfust_abi.cu"]
-HEADERS = ["cfust_device.cuh", "cfust_internal.h"]
+HEADERS = ["cfust_device.cuh", "cfust_internal.h", "cfust_special.cuh", "cfust_coeffs.h"]
 
 
 def nccl_paths() -> tuple[str, str]:

@@ -200,6 +200,7 @@ void cfust_destroy(cfust_ctx *ctx) {
     cudaFree(s.nu);
     cudaFree(s.comp);
     cudaFree(s.chi);
+    cudaFree(s.W);
     cudaFree(s.partials);
     cudaFree(s.stats);
     cudaFree(s.status);
@@ -252,6 +253,7 @@ int cfust_em_init(cfust_ctx **out, const double *y, int64_t n, int32_t p, int32_
         if (cudaGetDeviceProperties(&prop, ctx->device) != cudaSuccess) { rc = fail(ctx, CFUST_ECUDA, "cudaGetDeviceProperties"); break; }
         if (prop.major < 10) { rc = fail(ctx, CFUST_ECUDA, "libcfust is built for sm_100a (B200)"); break; }
         if (cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) != cudaSuccess) { rc = fail(ctx, CFUST_ECUDA, "stream"); break; }
+        if (upload_special_constants() != 0) { rc = fail(ctx, CFUST_ECUDA, "constant upload failed"); break; }
         for (auto &e : ctx->ev)
             if (cudaEventCreate(&e) != cudaSuccess) { rc = fail(ctx, CFUST_ECUDA, "event"); break; }
         if (rc != CFUST_OK) break;
@@ -272,6 +274,7 @@ int cfust_em_init(cfust_ctx **out, const double *y, int64_t n, int32_t p, int32_
                   alloc((void **)&s.delta, sizeof(double) * g * p * (q > 0 ? q : 1)) &&
                   alloc((void **)&s.nu, sizeof(double) * g) && alloc((void **)&s.comp, comp_dev_size() * g) &&
                   alloc((void **)&s.chi, sizeof(double) * g * 3 * (M > 0 ? M : 1)) &&
+                  alloc((void **)&s.W, sizeof(double) * (q > 0 ? q : 1) * (M > 0 ? M : 1)) &&
                   alloc((void **)&s.partials, sizeof(double) * size_t(max_partial_blocks(s)) * GK1) &&
                   alloc((void **)&s.stats, sizeof(double) * GK1) && alloc((void **)&s.status, sizeof(int) * 4) &&
                   alloc((void **)&ctx->d_ll, sizeof(double));
@@ -298,12 +301,12 @@ int cfust_em_init(cfust_ctx **out, const double *y, int64_t n, int32_t p, int32_
         if (rc != CFUST_OK) break;
         rc = upload_params(ctx, init);
         if (rc != CFUST_OK) break;
-        if (launch_check_finite(s.y, n * p, s.status + 2, ctx->stream) != 0 || launch_derive(s, ctx->stream) != 0 ||
-            launch_chi(s, ctx->stream) != 0) {
+        if (launch_check_finite(s.y, n * p, s.status + 2, ctx->stream) != 0 || launch_lattice(s, ctx->stream) != 0 ||
+            launch_derive(s, ctx->stream) != 0 || launch_chi(s, ctx->stream) != 0) {
             rc = fail(ctx, CFUST_ECUDA, cudaGetErrorString(cudaGetLastError()));
             break;
         }
-        ctx->launches += 3;
+        ctx->launches += 4;
         rc = fetch_status_and_sync(ctx);
         if (rc != CFUST_OK) break;
         if (ctx->world > 1) {

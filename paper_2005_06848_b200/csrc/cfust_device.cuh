@@ -7,6 +7,8 @@
 #include <cuda_runtime.h>
 #include <math_constants.h>
 
+#include "cfust_special.cuh"
+
 namespace cfust {
 
 constexpr int PMAX = 8;
@@ -46,9 +48,9 @@ __device__ __forceinline__ double lattice_w(const LatticeDev& L, int l, int k) {
 }
 
 // ------------------------------------------------------------------------------------------
-// Standard normal CDF / quantile (CUDA libdevice, FP64).
-__device__ __forceinline__ double Phi(double x) { return normcdf(x); }
-__device__ __forceinline__ double Phiinv(double u) { return normcdfinv(u); }
+// Standard normal CDF / quantile used by the SOV loop (cfust_special.cuh).
+__device__ __forceinline__ double Phi(double x) { return Phi_fast(x); }
+__device__ __forceinline__ double Phiinv(double u) { return Phiinv_fast(u); }
 
 // digamma: upward recurrence to x >= 16, then the Stirling-type asymptotic series.
 __device__ inline double dev_digamma(double x) {

@@ -19,6 +19,7 @@ struct DevState {
     double *pi, *mu, *sigma, *delta, *nu;   // Psi on device
     CompDev *comp;                  // [g]
     double *chi;                    // [g][3][M] chi radius nodes for df m0, m0+1, m0+2
+    double *W;                      // [q][M] lattice coordinates (fixed per context)
     double *partials;               // [max_blocks][g*K+1]
     double *stats;                  // [g*K+1] reduced (then all-reduced) statistics
     int *status;                    // [4]: 0 E-step underflow, 1 M-step/derive error code
@@ -36,8 +37,10 @@ int launch_reduce(const DevState &s, int nblocks, int mode, double *out, cudaStr
 int launch_mstep(const DevState &s, cudaStream_t st);
 int launch_derive(const DevState &s, cudaStream_t st);
 int launch_chi(const DevState &s, cudaStream_t st);
+int launch_lattice(const DevState &s, cudaStream_t st);
 int launch_check_finite(const double *y, int64_t count, int *flag, cudaStream_t st);
 size_t comp_dev_size();
+int upload_special_constants();
 int max_partial_blocks(const DevState &s);
 
 }  // namespace cfust

@@ -20,7 +20,14 @@
 
 namespace cfust {
 
-constexpr int EW = 8;            // warps per block of the CFUST E-step
+#ifndef CFUST_EW
+#define CFUST_EW 8
+#endif
+#ifndef CFUST_MINB
+#define CFUST_MINB 2
+#endif
+constexpr int EW = CFUST_EW;     // warps per block of the CFUST E-step
+constexpr int MINB = CFUST_MINB; // resident blocks per SM the register budget must allow
 constexpr int RW = 3 + QMAX + QMAX * QMAX;   // per-component result row in scratch
 
 // Per-warp scratch for the per-pair setup (written redundantly by all lanes with identical
@@ -45,36 +52,55 @@ struct WarpScratch {
 // SOV point loop for T_R (chi-normal form, reading R-T): this lane's share of
 //   sum_l prod_k Phi(a_k(l)),  a_0 = s_l binv_0,  a_k = s_l binv_k - sum_{t<k} Cn_kt z_t,
 //   z_t = Phi^{-1}(clamp(w_{l,t+1} e_t)).
+#ifndef CFUST_NPTS
+#define CFUST_NPTS 1
+#endif
+constexpr int NPTS = CFUST_NPTS;   // lattice points per lane per iteration (independent chains)
+
 template <int R>
 __device__ __forceinline__ double sov_lane_sum(const double (&binv)[R], const double (&Cn)[R * (R - 1) / 2],
-                                               const double *__restrict__ chi, const LatticeDev &L, int lane) {
-    double acc = 0.0;
-    for (int l = lane; l < L.M; l += 32) {
-        const double s = __ldg(chi + l);
-        double e = Phi(s * binv[0]);
-        double f = e;
-        double z[R - 1];
+                                               const double *__restrict__ chi, const double *__restrict__ W, int M,
+                                               int lane) {
+    // NPTS lattice points per iteration (l, l + 32, ...): independent chains for the FP64 pipe
+    double acc[NPTS];
+#pragma unroll
+    for (int j = 0; j < NPTS; ++j) acc[j] = 0.0;
+    for (int l0 = lane; l0 < M; l0 += 32 * NPTS) {
+        double s[NPTS], e[NPTS], f[NPTS], z[NPTS][R - 1];
+#pragma unroll
+        for (int j = 0; j < NPTS; ++j) {
+            s[j] = __ldg(chi + l0 + 32 * j);
+            e[j] = Phi(s[j] * binv[0]);
+            f[j] = e[j];
+        }
 #pragma unroll
         for (int k = 1; k < R; ++k) {
-            const double w = lattice_w(L, l, k);
-            const double u = fmin(fmax(w * e, UMIN), UMAX);
-            z[k - 1] = Phiinv(u);
-            double a = s * binv[k];
 #pragma unroll
-            for (int t = 0; t < k; ++t) a -= Cn[(k * (k - 1)) / 2 + t] * z[t];
-            e = Phi(a);
-            f *= e;
+            for (int j = 0; j < NPTS; ++j) {
+                const double w = __ldg(W + k * M + l0 + 32 * j);   // lattice coordinate k (table)
+                z[j][k - 1] = Phiinv(fmin(fmax(w * e[j], UMIN), UMAX));
+                double a = s[j] * binv[k];
+#pragma unroll
+                for (int t = 0; t < k; ++t) a -= Cn[(k * (k - 1)) / 2 + t] * z[j][t];
+                e[j] = Phi(a);
+                f[j] *= e[j];
+            }
         }
-        acc += f;
+#pragma unroll
+        for (int j = 0; j < NPTS; ++j) acc[j] += f[j];
     }
-    return acc;
+    double tot = 0.0;
+#pragma unroll
+    for (int j = 0; j < NPTS; ++j) tot += acc[j];
+    return tot;
 }
 
 // T_R(b; 0, S, m): R = 0 -> 1; R = 1 -> univariate t CDF; R >= 2 -> lattice rule with
 // univariate-prioritisation reordering (ascending b_k / sqrt(S_kk), stable; reading A13).
 template <int R>
-__device__ double T_eval(const double *b, const double *S, int lds, double m, const double *__restrict__ chi,
-                         const LatticeDev &L, int lane) {
+__device__ __noinline__ double T_eval(const double *b, const double *S, int lds, double m,
+                                      const double *__restrict__ chi, const double *__restrict__ W, int M,
+                                      int lane) {
     if constexpr (R == 0) {
         return 1.0;
     } else if constexpr (R == 1) {
@@ -109,15 +135,15 @@ __device__ double T_eval(const double *b, const double *S, int lds, double m, co
         for (int k = 1; k < R; ++k)
 #pragma unroll
             for (int t = 0; t < k; ++t) Cn[(k * (k - 1)) / 2 + t] = C[k][t] / C[k][k];
-        const double acc = sov_lane_sum<R>(binv, Cn, chi, L, lane);
-        return warp_sum(acc) / double(L.M);
+        const double acc = sov_lane_sum<R>(binv, Cn, chi, W, M, lane);
+        return warp_sum(acc) / double(M);
     }
 }
 
 // Per pair (observation in ws.y, component cp): O2-O8 of DESIGN.md §3.
 // MODE 1 computes only log f (T0).  Results go to res[] (identical in all lanes).
 template <int Q, int MODE>
-__device__ void pair_eval(const CompDev &cp, int p, const LatticeDev &L, const double *__restrict__ chi,
+__device__ void pair_eval(const CompDev &cp, int p, const double *__restrict__ W, int M, const double *__restrict__ chi,
                           WarpScratch &ws, double *res, int lane) {
     double r[PMAX], v[PMAX];
     double d = 0.0;
@@ -143,12 +169,11 @@ __device__ void pair_eval(const CompDev &cp, int p, const LatticeDev &L, const d
             if (a < p) s += cp.A[k * PMAX + a] * r[a];
         c[k] = s;
     }
-    const int M = L.M;
     // T0 (density, Eq. (2)) and T2 (for e2)
     const double sq0 = sqrt(m0 / rho);
 #pragma unroll
     for (int k = 0; k < Q; ++k) ws.b[k] = c[k] * sq0;
-    const double T0 = T_eval<Q>(ws.b, cp.Lam, QMAX, m0, chi, L, lane);
+    const double T0 = T_eval<Q>(ws.b, cp.Lam, QMAX, m0, chi, W, M, lane);
     if (MODE == 1) {
         res[0] = (T0 > 0.0) ? Q * CUDART_LN2 + logt + log(T0) : -CUDART_INF;
         return;
@@ -156,7 +181,7 @@ __device__ void pair_eval(const CompDev &cp, int p, const LatticeDev &L, const d
     const double sq2 = sqrt((m0 + 2.0) / rho);
 #pragma unroll
     for (int k = 0; k < Q; ++k) ws.b[k] = c[k] * sq2;
-    const double T2 = T_eval<Q>(ws.b, cp.Lam, QMAX, m0 + 2.0, chi + 2 * M, L, lane);
+    const double T2 = T_eval<Q>(ws.b, cp.Lam, QMAX, m0 + 2.0, chi + 2 * M, W, M, lane);
     res[1] = cp.psi_half_m0 - log(0.5 * rho) - m0 / rho;      // e1 - e2, reading A5
     if (!(T0 > 0.0)) {                                          // reading A16
         res[0] = -CUDART_INF;
@@ -216,7 +241,7 @@ __device__ void pair_eval(const CompDev &cp, int p, const LatticeDev &L, const d
                     }
                     ++ib;
                 }
-                const double val = T_eval<Q2>(ws.bc, ws.Sc, QMAX, m0, chi, L, lane);
+                const double val = T_eval<Q2>(ws.bc, ws.Sc, QMAX, m0, chi, W, M, lane);
                 ws.Tkt[k * QMAX + t] = val;
                 ws.Tkt[t * QMAX + k] = val;            // symmetric in {k, t} (A17)
             }
@@ -226,7 +251,7 @@ __device__ void pair_eval(const CompDev &cp, int p, const LatticeDev &L, const d
 #pragma unroll
     for (int k = 0; k < Q; ++k) {
         double tk = 1.0;
-        if constexpr (Q >= 2) tk = T_eval<Q1>(ws.ct[k], ws.St[k], QMAX, m0 + 1.0, chi + M, L, lane);
+        if constexpr (Q >= 2) tk = T_eval<Q1>(ws.ct[k], ws.St[k], QMAX, m0 + 1.0, chi + M, W, M, lane);
         ws.Tk[k] = tk;
         h[k] = ws.phi[k] * tk;
     }
@@ -317,7 +342,8 @@ struct EArgs {
     int p, g, K;
     const CompDev *__restrict__ comp;
     const double *__restrict__ chi;
-    LatticeDev lat;
+    const double *__restrict__ W;   // [q][M] lattice coordinates w_{l,k}
+    int M;
     double *__restrict__ partials;
     int *status;
     const int64_t *__restrict__ idx;
@@ -327,7 +353,7 @@ struct EArgs {
 
 // MODE 0: E-step statistics; 1: log-likelihood only; 2: per-pair dump of idx[0..cnt).
 template <int Q, int MODE>
-__global__ void __launch_bounds__(EW * 32) estep_cfust_kernel(EArgs A) {
+__global__ void __launch_bounds__(EW * 32, MINB) estep_cfust_kernel(EArgs A) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const int p = A.p, g = A.g, K = A.K, GK = g * K;
@@ -342,7 +368,7 @@ __global__ void __launch_bounds__(EW * 32) estep_cfust_kernel(EArgs A) {
     __syncthreads();
     WarpScratch &ws = wsa[wid];
     double *acc = acc_all + wid * (GK + 1);
-    const int M = A.lat.M;
+    const int M = A.M;
     const int64_t nwarps = int64_t(gridDim.x) * EW;
     const int64_t total = (MODE == 2) ? A.cnt : A.n;
     double ll = 0.0;
@@ -352,7 +378,7 @@ __global__ void __launch_bounds__(EW * 32) estep_cfust_kernel(EArgs A) {
         if (lane < p) ws.y[lane] = A.y[j * p + lane];
         __syncwarp();
         for (int i = 0; i < g; ++i)
-            pair_eval<Q, MODE == 1 ? 1 : 0>(comp[i], p, A.lat, A.chi + size_t(i) * 3 * M, ws, ws.res[i], lane);
+            pair_eval<Q, MODE == 1 ? 1 : 0>(comp[i], p, A.W, M, A.chi + size_t(i) * 3 * M, ws, ws.res[i], lane);
         __syncwarp();
         // Eq. (3)-(4): LSE over components, tau
         double lf[GMAX], mx = -CUDART_INF;
@@ -625,6 +651,7 @@ __device__ int derive_one(const DevState &s, int i, CompDev &cd) {
     const double *Sg = s.sigma + size_t(i) * p * p;
     const double *D = s.delta + size_t(i) * p * q;
     double Om[PMAX * PMAX];
+    if (!chol_dev(p, Sg, p, Om, PMAX)) return -4;   // Sigma itself must be PD
     for (int a = 0; a < p; ++a)
         for (int b = 0; b < p; ++b) {
             double v = Sg[a * p + b];
@@ -783,14 +810,22 @@ __global__ void mstep_kernel(DevState s) {
 }
 
 // chi radius nodes: chi[(i*3 + k)*M + l] = sqrt(chi2_{m0+k}^{-1}(w_{l,0}) / (m0+k))
-__global__ void chi_kernel(DevState s, LatticeDev L) {
-    const int total = s.g * 3 * L.M;
+__global__ void chi_kernel(DevState s) {
+    const int M = s.M;
+    const int total = s.g * 3 * M;
     for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < total; t += gridDim.x * blockDim.x) {
-        const int l = t % L.M, ik = t / L.M, i = ik / 3, k = ik % 3;
+        const int l = t % M, ik = t / M, i = ik / 3, k = ik % 3;
         const double m = s.comp[i].m0 + double(k);
-        const double w = lattice_w(L, l, 0);
+        const double w = s.W[l];   // coordinate 0 drives the chi radius
         s.chi[t] = sqrt(dev_chi2_quantile(w, m) / m);
     }
+}
+
+// lattice coordinates W[k][l] = |2 frac((l z_k mod M)/M + shift_k) - 1|, once per context
+__global__ void lattice_kernel(DevState s, LatticeDev L) {
+    const int total = s.q * s.M;
+    for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < total; t += gridDim.x * blockDim.x)
+        s.W[t] = lattice_w(L, t % s.M, t / s.M);
 }
 
 __global__ void check_finite_kernel(const double *__restrict__ y, int64_t count, int *flag) {
@@ -808,6 +843,16 @@ static LatticeDev make_lattice(const DevState &s) {
 }
 
 size_t comp_dev_size() { return sizeof(CompDev); }
+
+// Fill the special-function coefficient tables of this module's constant bank.
+int upload_special_constants() {
+    cudaError_t e;
+    if ((e = cudaMemcpyToSymbol(c_PH_P, h_PH_P, sizeof(h_PH_P))) != cudaSuccess) return int(e);
+    if ((e = cudaMemcpyToSymbol(c_PH_Q, h_PH_Q, sizeof(h_PH_Q))) != cudaSuccess) return int(e);
+    if ((e = cudaMemcpyToSymbol(c_NI_P, h_NI_P, sizeof(h_NI_P))) != cudaSuccess) return int(e);
+    if ((e = cudaMemcpyToSymbol(c_NI_Q, h_NI_Q, sizeof(h_NI_Q))) != cudaSuccess) return int(e);
+    return 0;
+}
 
 static size_t cfust_smem(const DevState &s) {
     const int GK = s.g * s.K;
@@ -885,7 +930,8 @@ int launch_estep(const DevState &s, int mode, const int64_t *idx, int64_t cnt, d
     a.K = s.K;
     a.comp = s.comp;
     a.chi = s.chi;
-    a.lat = make_lattice(s);
+    a.W = s.W;
+    a.M = s.M;
     a.partials = s.partials;
     a.status = s.status;
     a.idx = idx;
@@ -940,9 +986,16 @@ int launch_derive(const DevState &s, cudaStream_t st) {
 
 int launch_chi(const DevState &s, cudaStream_t st) {
     if (s.q < 2 || s.M <= 0) return 0;
-    const LatticeDev L = make_lattice(s);
     const int total = s.g * 3 * s.M;
-    chi_kernel<<<(total + 127) / 128, 128, 0, st>>>(s, L);
+    chi_kernel<<<(total + 127) / 128, 128, 0, st>>>(s);
+    return int(cudaGetLastError());
+}
+
+int launch_lattice(const DevState &s, cudaStream_t st) {
+    if (s.q < 2 || s.M <= 0) return 0;
+    const LatticeDev L = make_lattice(s);
+    const int total = s.q * s.M;
+    lattice_kernel<<<(total + 127) / 128, 128, 0, st>>>(s, L);
     return int(cudaGetLastError());
 }
 

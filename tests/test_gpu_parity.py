@@ -134,7 +134,7 @@ def test_estep_stats_and_loglik_parity(cf, orc, cfg_id, n):
 
 
 # ------------------------------------------------------------------ full EM parity
-FIT_CASES = [(1, 1000, 10), (2, 150, 10), (3, 20000, 10), (4, 16, 5), (5, 200, 5)]
+FIT_CASES = [(1, 1000, 10), (2, 150, 10), (3, 20000, 10), (4, 120, 5), (5, 200, 5)]
 
 
 @pytest.mark.parametrize("cfg_id,n,iters", FIT_CASES)
