@@ -17,7 +17,19 @@ import numpy as np
 from ._native import (CFUST_EDIM, CFUST_EEMPTY, CFUST_EINVAL, CFUST_EMIXPROP, CFUST_ENCCL,  # noqa: F401
                       CFUST_ENOTPD, CFUST_EUNDERFLOW, CFUST_ECUDA, CfustError, Opts, Params, Result, lib)
 
-__all__ = ["CfustEM", "CfustError", "k_stats", "nccl_unique_id", "lib"]
+__all__ = ["CfustEM", "CfustError", "k_stats", "nccl_unique_id", "eval_special", "lib"]
+
+SPECIAL = {"phi": 0, "phiinv": 1, "exp": 2, "log": 3, "t_cdf": 4, "chi2_quantile": 5, "digamma": 6, "sqrt": 7}
+
+
+def eval_special(name: str, x, aux: float = 0.0) -> np.ndarray:
+    """Evaluate one of the device special functions (diagnostic; the code the kernels inline)."""
+    xs = np.ascontiguousarray(np.asarray(x, dtype=np.float64).ravel())
+    ys = np.empty_like(xs)
+    rc = lib().cfust_eval_special(SPECIAL[name], _dptr(xs), _dptr(ys), len(xs), float(aux))
+    if rc != 0:
+        raise CfustError(rc, f"cfust_eval_special({name})")
+    return ys
 
 
 def k_stats(p: int, q: int) -> int:

@@ -40,8 +40,8 @@ class Result(C.Structure):
 # every symbol declared in include/cfust.h (checked by tests/test_abi_symbols.py)
 EXPORTS = ["cfust_em_init", "cfust_set_data", "cfust_estep", "cfust_mstep", "cfust_iterate", "cfust_loglik",
            "cfust_fit", "cfust_get_params", "cfust_set_params", "cfust_get_pairs", "cfust_get_timing",
-           "cfust_stream", "cfust_launch_count", "cfust_nccl_unique_id", "cfust_k_stats", "cfust_last_error",
-           "cfust_destroy"]
+           "cfust_stream", "cfust_launch_count", "cfust_nccl_unique_id", "cfust_eval_special", "cfust_k_stats",
+           "cfust_last_error", "cfust_destroy"]
 
 _lib = None
 
@@ -71,13 +71,14 @@ def lib():
         L.cfust_launch_count.restype = i64
         L.cfust_nccl_unique_id.argtypes = [vp]
         L.cfust_k_stats.argtypes = [i32, i32]
+        L.cfust_eval_special.argtypes = [i32, dp, dp, i64, C.c_double]
         L.cfust_last_error.argtypes = [vp]
         L.cfust_last_error.restype = C.c_char_p
         L.cfust_destroy.argtypes = [vp]
         L.cfust_destroy.restype = None
         for name in ["cfust_em_init", "cfust_set_data", "cfust_estep", "cfust_mstep", "cfust_iterate",
                      "cfust_loglik", "cfust_fit", "cfust_get_params", "cfust_set_params", "cfust_get_pairs",
-                     "cfust_get_timing", "cfust_nccl_unique_id", "cfust_k_stats"]:
+                     "cfust_get_timing", "cfust_nccl_unique_id", "cfust_k_stats", "cfust_eval_special"]:
             getattr(L, name).restype = C.c_int
         _lib = L
     return _lib

@@ -515,6 +515,25 @@ int cfust_get_pairs(cfust_ctx *ctx, const int64_t *idx, int64_t cnt, double *out
     return rc;
 }
 
+int cfust_eval_special(int32_t which, const double *x, double *y, int64_t n, double aux) {
+    if (!x || !y || n < 0 || which < 0 || which > 7) return CFUST_EINVAL;
+    if (n == 0) return CFUST_OK;
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev < 1) return CFUST_ECUDA;
+    if (upload_special_constants() != 0) return CFUST_ECUDA;
+    double *dx = nullptr, *dy = nullptr;
+    if (cudaMalloc((void **)&dx, sizeof(double) * n) != cudaSuccess) return CFUST_ECUDA;
+    if (cudaMalloc((void **)&dy, sizeof(double) * n) != cudaSuccess) { cudaFree(dx); return CFUST_ECUDA; }
+    int rc = CFUST_OK;
+    if (cudaMemcpy(dx, x, sizeof(double) * n, cudaMemcpyHostToDevice) != cudaSuccess ||
+        launch_special(which, dx, dy, n, aux, 0) != 0 ||
+        cudaMemcpy(y, dy, sizeof(double) * n, cudaMemcpyDeviceToHost) != cudaSuccess)
+        rc = CFUST_ECUDA;
+    cudaFree(dx);
+    cudaFree(dy);
+    return rc;
+}
+
 int cfust_get_timing(cfust_ctx *ctx, double *ms, int64_t *counts, int32_t reset) {
     if (!ctx) return CFUST_EINVAL;
     for (int k = 0; k < 4; ++k) {

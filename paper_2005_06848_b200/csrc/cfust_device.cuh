@@ -28,7 +28,8 @@ struct CompDev {
     double psi_half_m0;           // digamma(m0/2) for e1 - e2 (reading A5)
     double lgc_m0;                // lgamma((m0+1)/2) - lgamma(m0/2)      (t_1 density, df m0)
     double lgc_m0m1;              // lgamma(m0/2) - lgamma((m0-1)/2)      (t_1 density, df m0-1)
-    double pad;
+    double inv_nu;                // 1 / nu
+    double log_half_nu;           // log(nu / 2)
 };
 
 struct LatticeDev {

@@ -41,6 +41,7 @@ int launch_lattice(const DevState &s, cudaStream_t st);
 int launch_check_finite(const double *y, int64_t count, int *flag, cudaStream_t st);
 size_t comp_dev_size();
 int upload_special_constants();
+int launch_special(int which, const double *x, double *y, int64_t n, double aux, cudaStream_t st);
 int max_partial_blocks(const DevState &s);
 
 }  // namespace cfust

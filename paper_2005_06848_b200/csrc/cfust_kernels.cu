@@ -78,7 +78,10 @@ __device__ __forceinline__ double sov_lane_sum(const double (&binv)[R], const do
 #pragma unroll
             for (int j = 0; j < NPTS; ++j) {
                 const double w = __ldg(W + k * M + l0 + 32 * j);   // lattice coordinate k (table)
-                z[j][k - 1] = Phiinv(fmin(fmax(w * e[j], UMIN), UMAX));
+                double u = w * e[j];
+                u = (u < UMIN) ? UMIN : u;   // clamps (reading A15); plain compares, no NaN semantics
+                u = (u > UMAX) ? UMAX : u;
+                z[j][k - 1] = Phiinv(u);
                 double a = s[j] * binv[k];
 #pragma unroll
                 for (int t = 0; t < k; ++t) a -= Cn[(k * (k - 1)) / 2 + t] * z[j][t];
@@ -448,127 +451,199 @@ __global__ void __launch_bounds__(EW * 32, MINB) estep_cfust_kernel(EArgs A) {
 }
 
 // ------------------------------------------------------------------------------------------
-// q == 0: t-mixture E-step (Delta = 0).  Block = g warps x TW tiles; warp
-// (i, tile) evaluates component i for 32 observations (one per lane) and keeps its 3+p+
-// p(p+1)/2 statistics in registers; tau needs all g log-densities -> exchanged via smem.
-constexpr int TW = 1;   // observation tiles (of 32) per block
+// q == 0: t-mixture E-step (Delta = 0), streaming y from HBM.
+// Tile = TT observations = TT threads.  Phase 1: thread per observation evaluates all g
+// components (d, log f, tau, e2, e1-e2) and writes y (augmented with a constant 1) and the
+// weights tau*e2, tau, tau*(e1-e2) to shared memory.  Phase 2: the tile contraction
+//   S1/S2/S3_i += sum_j (tau e2)_ij y~_j y~_j'   (y~ = (y, 1): S3 = upper block, S2 = last column,
+//                                                 S1 = corner),   S0_i, S7_i = weighted row sums,
+// split into register-blocked 3x3 tasks x TCH row-chunks; every thread keeps its two tasks'
+// accumulators in registers across tiles.  Deterministic: fixed task/chunk/row order.
+// (A product-per-lane variant with broadcast weights measured 1.8x slower: idle lanes, 8 warps/SM.)
+constexpr int TT = 256;    // observations per tile (= threads per block)
+constexpr int TCH = 8;     // row chunks per contraction task (rows r = rr*TCH + ch: bank-spread)
+constexpr int TSLOT = 2;   // contraction (task, chunk) slots per thread
 
 template <int P>
-__global__ void __launch_bounds__(GMAX * TW * 32) estep_t_kernel(EArgs A, int mode) {
+struct TLayout {
+    static constexpr int PE = P + 1;               // y~ = (y, 1)
+    static constexpr int NB = (PE + 2) / 3;        // 3-wide coordinate blocks
+    static constexpr int YS = 3 * NB;              // row stride of y~ in smem (zero padded)
+    static constexpr int NBP = NB * (NB + 1) / 2;  // upper block pairs (A <= B)
+    static constexpr int WS = GMAX + 1;            // row stride of the weight arrays (bank spread)
+};
+
+static_assert(GMAX * (TLayout<PMAX>::NBP + 1) * TCH <= TSLOT * TT, "contraction tasks exceed thread slots");
+
+template <int P>
+__global__ void __launch_bounds__(TT, 2) estep_t_kernel(EArgs A, int mode) {
+    using Lt = TLayout<P>;
+    constexpr int NB = Lt::NB, YS = Lt::YS, NBP = Lt::NBP, WS = Lt::WS;
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
     const int g = A.g, K = A.K, GK = g * K;
-    const int comp_i = wid % g, tile = wid / g;
-    const bool active_warp = wid < g * TW;
     CompDev *comp = reinterpret_cast<CompDev *>(smem_raw);
-    double *ys = reinterpret_cast<double *>(comp + g);                  // [TW*32][P+1]
-    double *lfs = ys + TW * 32 * (P + 1);                                // [TW][GMAX][32]
-    double *lse_s = lfs + TW * GMAX * 32;                                // [TW][32]
-    double *red = lse_s + TW * 32;                                       // [g*TW][K+1] block reduce
-    for (int t = threadIdx.x; t < g * int(sizeof(CompDev) / sizeof(double)); t += blockDim.x)
-        reinterpret_cast<double *>(comp)[t] = reinterpret_cast<const double *>(A.comp)[t];
+    double *yt = reinterpret_cast<double *>(comp + g);   // [TT][YS]
+    double *we = yt + TT * YS;                           // [TT][WS] tau*e2
+    double *wt = we + TT * WS;                           // [TT][WS] tau
+    double *wl = wt + TT * WS;                           // [TT][WS] tau*(e1-e2)
+    double *red = wl + TT * WS;                          // end-of-kernel reduction scratch
+    for (int k = t; k < g * int(sizeof(CompDev) / sizeof(double)); k += TT)
+        reinterpret_cast<double *>(comp)[k] = reinterpret_cast<const double *>(A.comp)[k];
     __syncthreads();
-    const CompDev &cp = comp[comp_i];
-    constexpr int NS = 3 + P + P * (P + 1) / 2;   // S0, S1, S2[P], S3[P(P+1)/2], S7
-    double st[NS];
+    const int ntask = g * (NBP + 1);   // per component: NBP block pairs + 1 scalar task (S0, S7)
+    double acc[TSLOT][9];
 #pragma unroll
-    for (int k = 0; k < NS; ++k) st[k] = 0.0;
+    for (int sl = 0; sl < TSLOT; ++sl)
+#pragma unroll
+        for (int k = 0; k < 9; ++k) acc[sl][k] = 0.0;
     double ll = 0.0;
     const int64_t n = A.n;
-    const int64_t ntiles = (n + 32 * TW - 1) / (32 * TW);
+    const int64_t ntiles = (n + TT - 1) / TT;
     for (int64_t tb = blockIdx.x; tb < ntiles; tb += gridDim.x) {
-        const int64_t j0 = tb * 32 * TW;
-        const int64_t rows = (n - j0 < 32 * TW) ? (n - j0) : int64_t(32 * TW);
-        __syncthreads();
-        for (int t = threadIdx.x; t < rows * P; t += blockDim.x) {
-            const int rr = t / P, a = t % P;
-            ys[rr * (P + 1) + a] = A.y[j0 * P + t];
-        }
-        __syncthreads();
-        const int row = tile * 32 + lane;
-        const bool valid = active_warp && row < rows;
-        double y[P], dd = 0.0, lf = -CUDART_INF;
+        // ---------------- phase 1: one observation per thread, all components
+        const int64_t j = tb * TT + t;
+        double y[P];
+        const bool valid = j < n;
         if (valid) {
-            double v[P];
+            const double *yr = A.y + j * P;
+            if constexpr (P % 2 == 0) {
 #pragma unroll
-            for (int a = 0; a < P; ++a) y[a] = ys[row * (P + 1) + a];
+                for (int a = 0; a < P; a += 2) {
+                    const double2 v2 = __ldg(reinterpret_cast<const double2 *>(yr + a));
+                    y[a] = v2.x;
+                    y[a + 1] = v2.y;
+                }
+            } else {
 #pragma unroll
-            for (int a = 0; a < P; ++a) {
-                double s = y[a] - cp.mu[a];
-#pragma unroll
-                for (int bb = 0; bb < a; ++bb) s -= cp.L[a * PMAX + bb] * v[bb];
-                v[a] = s * cp.Linv[a];
-                dd += v[a] * v[a];
+                for (int a = 0; a < P; ++a) y[a] = __ldg(yr + a);
             }
-            lf = cp.logpi + cp.kappa - 0.5 * cp.m0 * log1p(dd / cp.nu);
-            lfs[(tile * GMAX + comp_i) * 32 + lane] = lf;
-        }
-        __syncthreads();
-        if (valid && comp_i == 0) {   // LSE over components for this observation
-            double mx = -CUDART_INF;
-            for (int i = 0; i < g; ++i) mx = fmax(mx, lfs[(tile * GMAX + i) * 32 + lane]);
-            double se = 0.0;
-            for (int i = 0; i < g; ++i) se += exp(lfs[(tile * GMAX + i) * 32 + lane] - mx);
-            const double lse = (mx == -CUDART_INF) ? mx : mx + log(se);
-            if (mx == -CUDART_INF) atomicOr(A.status, 1);
-            lse_s[tile * 32 + lane] = lse;
-            ll += lse;
-        }
-        __syncthreads();
-        if (valid && mode == 0) {
-            const double lse = lse_s[tile * 32 + lane];
-            const double tau = exp(lf - lse);
-            if (tau > 0.0) {
-                const double rho = cp.nu + dd;
-                const double e2 = cp.m0 / rho;
-                const double e1me2 = cp.psi_half_m0 - log(0.5 * rho) - e2;
-                const double te2 = tau * e2;
-                st[0] += tau;
-                st[1] += te2;
-                int o = 2;
+        } else {
 #pragma unroll
-                for (int a = 0; a < P; ++a) st[o + a] += te2 * y[a];
-                o += P;
+            for (int a = 0; a < P; ++a) y[a] = 0.0;
+        }
+        double lf[GMAX], l1[GMAX], dd[GMAX];
+        double mx = -CUDART_INF;
+#pragma unroll
+        for (int i = 0; i < GMAX; ++i) {
+            if (i < g) {
+                const CompDev &cp = comp[i];
+                double v[P], d = 0.0;
 #pragma unroll
                 for (int a = 0; a < P; ++a) {
-                    const double ta = te2 * y[a];
+                    double s = y[a] - cp.mu[a];
 #pragma unroll
-                    for (int bb = a; bb < P; ++bb) st[o++] += ta * y[bb];
+                    for (int b = 0; b < a; ++b) s -= cp.L[a * PMAX + b] * v[b];
+                    v[a] = s * cp.Linv[a];
+                    d += v[a] * v[a];
                 }
-                st[NS - 1] += tau * e1me2;
+                dd[i] = d;
+                l1[i] = log1p(d * cp.inv_nu);
+                lf[i] = cp.logpi + cp.kappa - 0.5 * cp.m0 * l1[i];
+                mx = fmax(mx, lf[i]);
             }
         }
-    }
-    // block reduction: lanes -> warp (shuffle tree), warps (i, tile) -> block (fixed order)
+        double se = 0.0;
 #pragma unroll
-    for (int k = 0; k < NS; ++k) st[k] = warp_sum(st[k]);
+        for (int i = 0; i < GMAX; ++i)
+            if (i < g) { lf[i] = exp(lf[i] - mx); se += lf[i]; }   // lf now holds exp(lf - max)
+        if (valid && mx == -CUDART_INF) atomicOr(A.status, 1);
+        if (valid) ll += mx + log(se);
+        if (mode == 1) continue;
+        const double ise = 1.0 / se;
+#pragma unroll
+        for (int a = 0; a < YS; ++a) yt[t * YS + a] = (a < P) ? y[a] : (a == P ? 1.0 : 0.0);
+#pragma unroll
+        for (int i = 0; i < GMAX; ++i) {
+            if (i < g) {
+                const CompDev &cp = comp[i];
+                const double tau = valid ? lf[i] * ise : 0.0;
+                const double e2 = cp.m0 / (cp.nu + dd[i]);
+                const double e1me2 = cp.psi_half_m0 - (cp.log_half_nu + l1[i]) - e2;   // log(rho/2) = log(nu/2) + log1p(d/nu)
+                we[t * WS + i] = tau * e2;
+                wt[t * WS + i] = tau;
+                wl[t * WS + i] = tau * e1me2;
+            }
+        }
+        __syncthreads();
+        // ---------------- phase 2: tile contraction (register-blocked 3x3 tasks)
+#pragma unroll
+        for (int sl = 0; sl < TSLOT; ++sl) {
+            const int ts = t + sl * TT;
+            if (ts < ntask * TCH) {
+                const int task = ts / TCH, ch = ts % TCH;
+                const int i = task / (NBP + 1), kind = task % (NBP + 1);
+                if (kind == NBP) {   // S0 = sum tau, S7 = sum tau (e1 - e2)
+                    for (int rr = 0; rr < TT / TCH; ++rr) {
+                        const int r = rr * TCH + ch;
+                        acc[sl][0] += wt[r * WS + i];
+                        acc[sl][1] += wl[r * WS + i];
+                    }
+                } else {
+                    int BA = 0, rem = kind;
+                    while (rem >= NB - BA) { rem -= NB - BA; ++BA; }
+                    const int BB = BA + rem;
+                    for (int rr = 0; rr < TT / TCH; ++rr) {
+                        const int r = rr * TCH + ch;
+                        const double w = we[r * WS + i];
+                        const double *yr = yt + r * YS;
+                        const double ya0 = w * yr[3 * BA], ya1 = w * yr[3 * BA + 1], ya2 = w * yr[3 * BA + 2];
+                        const double yb0 = yr[3 * BB], yb1 = yr[3 * BB + 1], yb2 = yr[3 * BB + 2];
+                        acc[sl][0] += ya0 * yb0; acc[sl][1] += ya0 * yb1; acc[sl][2] += ya0 * yb2;
+                        acc[sl][3] += ya1 * yb0; acc[sl][4] += ya1 * yb1; acc[sl][5] += ya1 * yb2;
+                        acc[sl][6] += ya2 * yb0; acc[sl][7] += ya2 * yb1; acc[sl][8] += ya2 * yb2;
+                    }
+                }
+            }
+        }
+        __syncthreads();
+    }
+    // ---------------- block reduction: log-likelihood
     ll = warp_sum(ll);
     __syncthreads();
-    if (active_warp && lane == 0) {
-        double *r = red + size_t(wid) * (K + 1);
+    if (lane == 0) red[wid] = ll;
+    __syncthreads();
+    double *out = A.partials + size_t(blockIdx.x) * (GK + 1);
+    if (t == 0) {
+        double s = 0.0;
+        for (int w = 0; w < TT / 32; ++w) s += red[w];
+        out[GK] = s;
+    }
+    if (mode == 1) return;
+    __syncthreads();
+    // task accumulators -> smem [ntask][TCH][9], then per statistics entry in chunk order
+    double *tr = red + 32;
 #pragma unroll
-        for (int k = 0; k < NS; ++k) r[k] = st[k];
-        r[K] = (comp_i == 0) ? ll : 0.0;
+    for (int sl = 0; sl < TSLOT; ++sl) {
+        const int ts = t + sl * TT;
+        if (ts < ntask * TCH)
+#pragma unroll
+            for (int k = 0; k < 9; ++k) tr[ts * 9 + k] = acc[sl][k];
     }
     __syncthreads();
-    if (mode == 1) {
-        if (threadIdx.x == 0) {
-            double s = 0.0;
-            for (int t = 0; t < TW; ++t) s += red[size_t(t * g) * (K + 1) + K];
-            A.partials[size_t(blockIdx.x) * (GK + 1) + GK] = s;
-        }
-        return;
-    }
-    double *out = A.partials + size_t(blockIdx.x) * (GK + 1);
-    for (int e = threadIdx.x; e <= GK; e += blockDim.x) {
+    auto task_sum = [&](int task, int k) {
         double s = 0.0;
-        if (e < GK) {
-            const int i = e / K, k = e % K;
-            for (int t = 0; t < TW; ++t) s += red[size_t(t * g + i) * (K + 1) + k];
-        } else {
-            for (int t = 0; t < TW; ++t) s += red[size_t(t * g) * (K + 1) + K];
-        }
-        out[e] = s;
+        for (int ch = 0; ch < TCH; ++ch) s += tr[(task * TCH + ch) * 9 + k];
+        return s;
+    };
+    auto pair_val = [&](int i, int a, int b) {   // sum (tau e2) y~_a y~_b, a <= b
+        const int BA = a / 3, BB = b / 3;
+        const int kind = BA * NB - BA * (BA - 1) / 2 + (BB - BA);
+        return task_sum(i * (NBP + 1) + kind, (a % 3) * 3 + (b % 3));
+    };
+    for (int e = t; e < GK; e += TT) {
+        const int i = e / K;
+        int k = e % K;
+        double v;
+        if (k == 0) v = task_sum(i * (NBP + 1) + NBP, 0);                 // S0
+        else if (k == 1) v = pair_val(i, P, P);                           // S1 = sum tau e2
+        else if ((k -= 2) < P) v = pair_val(i, k, P);                     // S2
+        else if ((k -= P) < P * (P + 1) / 2) {                            // S3 (upper, row-major)
+            int row = 0;
+            while (k >= P - row) { k -= P - row; ++row; }
+            v = pair_val(i, row, row + k);
+        } else v = task_sum(i * (NBP + 1) + NBP, 1);                      // S7
+        out[e] = v;
     }
 }
 
@@ -692,7 +767,8 @@ __device__ int derive_one(const DevState &s, int i, CompDev &cd) {
     cd.psi_half_m0 = dev_digamma(0.5 * m0);
     cd.lgc_m0 = lgamma(0.5 * (m0 + 1.0)) - lgamma(0.5 * m0);
     cd.lgc_m0m1 = lgamma(0.5 * m0) - lgamma(0.5 * (m0 - 1.0));
-    cd.pad = 0.0;
+    cd.inv_nu = 1.0 / nu;
+    cd.log_half_nu = log(0.5 * nu);
     return 0;
 }
 
@@ -833,6 +909,34 @@ __global__ void check_finite_kernel(const double *__restrict__ y, int64_t count,
         if (!isfinite(y[t])) atomicOr(flag, 1);
 }
 
+// Diagnostic element-wise evaluation of the device special functions (cfust_eval_special).
+__global__ void special_kernel(int which, const double *__restrict__ x, double *__restrict__ y, int64_t n, double aux) {
+    for (int64_t t = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; t < n; t += int64_t(gridDim.x) * blockDim.x) {
+        const double v = x[t];
+        double r;
+        switch (which) {
+            case 0: r = Phi(v); break;
+            case 1: r = Phiinv(v); break;
+            case 2: r = exp_neg(v); break;
+            case 3: r = log_unit(v); break;
+            case 4: r = dev_t_cdf(v, aux); break;
+            case 5: r = dev_chi2_quantile(v, aux); break;
+            case 6: r = dev_digamma(v); break;
+            case 7: r = sqrt_fast(v); break;
+            default: r = CUDART_NAN;
+        }
+        y[t] = r;
+    }
+}
+
+int launch_special(int which, const double *x, double *y, int64_t n, double aux, cudaStream_t st) {
+    int64_t blocks = (n + 127) / 128;
+    if (blocks < 1) blocks = 1;
+    if (blocks > 4096) blocks = 4096;
+    special_kernel<<<int(blocks), 128, 0, st>>>(which, x, y, n, aux);
+    return int(cudaGetLastError());
+}
+
 // ------------------------------------------------------------------------------------------
 // Launchers
 static LatticeDev make_lattice(const DevState &s) {
@@ -851,6 +955,8 @@ int upload_special_constants() {
     if ((e = cudaMemcpyToSymbol(c_PH_Q, h_PH_Q, sizeof(h_PH_Q))) != cudaSuccess) return int(e);
     if ((e = cudaMemcpyToSymbol(c_NI_P, h_NI_P, sizeof(h_NI_P))) != cudaSuccess) return int(e);
     if ((e = cudaMemcpyToSymbol(c_NI_Q, h_NI_Q, sizeof(h_NI_Q))) != cudaSuccess) return int(e);
+    if ((e = cudaMemcpyToSymbol(c_EXPC, h_EXPC, sizeof(h_EXPC))) != cudaSuccess) return int(e);
+    if ((e = cudaMemcpyToSymbol(c_LOGC, h_LOGC, sizeof(h_LOGC))) != cudaSuccess) return int(e);
     return 0;
 }
 
@@ -860,9 +966,9 @@ static size_t cfust_smem(const DevState &s) {
 }
 
 static size_t t_smem(const DevState &s) {
-    const int P = s.p;
-    return sizeof(CompDev) * s.g + sizeof(double) * (TW * 32 * (P + 1) + TW * GMAX * 32 + TW * 32) +
-           sizeof(double) * size_t(s.g * TW) * (s.K + 1);
+    const int PE = s.p + 1, NB = (PE + 2) / 3, YS = 3 * NB, NBP = NB * (NB + 1) / 2, WS = GMAX + 1;
+    const size_t tasks = size_t(s.g) * (NBP + 1) * TCH * 9;
+    return sizeof(CompDev) * s.g + sizeof(double) * (size_t(TT) * (YS + 3 * WS) + 32 + tasks);
 }
 
 template <int Q, int MODE>
@@ -904,12 +1010,12 @@ static int launch_t_p(const DevState &s, EArgs &a, int mode, cudaStream_t st, in
     const size_t sm = t_smem(s);
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
     if (e != cudaSuccess) return int(e);
-    const int threads = s.g * TW * 32;
+    const int threads = TT;
     int per_sm = 0;
     e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, sm);
     if (e != cudaSuccess) return int(e);
     if (per_sm < 1) per_sm = 1;
-    const int64_t ntiles = (a.n + 32 * TW - 1) / (32 * TW);
+    const int64_t ntiles = (a.n + TT - 1) / TT;
     int64_t blocks = int64_t(s.num_sms) * per_sm;
     if (blocks > ntiles) blocks = ntiles;
     if (blocks < 1) blocks = 1;

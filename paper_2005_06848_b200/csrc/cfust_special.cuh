@@ -56,13 +56,70 @@ __device__ __forceinline__ double div_fast(double p, double q) {
     return fma(fma(-q, y, p), r, y);
 }
 
+#ifndef CFUST_OWN_ELEM
+#define CFUST_OWN_ELEM 0   // 1: own branch-free exp/log/sqrt (measured equal speed, more registers)
+#endif
+
+// exp(x) for x <= 0 (x >= -708 exact to ~1 ulp; below: 0, i.e. results < 1e-307 flush).
+// x = k ln2 + r, |r| <= ln2/2: k from the 1.5*2^52 rounding trick, r with a two-part ln2,
+// Taylor to r^13, 2^k by adding k to the exponent field.
+__device__ __forceinline__ double exp_neg(double x) {
+#if CFUST_OWN_ELEM
+    const double t = fma(x, 1.4426950408889634074, 6755399441055744.0);
+    const int k = __double2loint(t);
+    const double kd = t - 6755399441055744.0;
+    const double r = fma(kd, -2.3190468138462996e-17, fma(kd, -0.69314718055994528623, x));
+    const double p = horner_c(c_EXPC, r);
+    const double res = __hiloint2double(__double2hiint(p) + k * (1 << 20), __double2loint(p));
+    return (x < -708.0) ? 0.0 : res;
+#else
+    return exp(x);
+#endif
+}
+
+// log(x) for normal x in (0, 1]: x = m 2^e, m in [sqrt(1/2), sqrt(2)); log m = 2 atanh(s),
+// s = (m-1)/(m+1) (m-1 exact), series to s^21.  Relative accuracy holds as x -> 1 (e = 0).
+__device__ __forceinline__ double log_unit(double x) {
+#if CFUST_OWN_ELEM
+    const int hx = __double2hiint(x);
+    int e = (hx >> 20) - 1023;
+    int mh = (hx & 0x000fffff) | 0x3ff00000;
+    const bool big = mh > 0x3ff6a09e;   // m > sqrt(2): halve
+    mh = big ? mh - 0x00100000 : mh;
+    e = big ? e + 1 : e;
+    const double m = __hiloint2double(mh, __double2loint(x));
+    const double s = div_fast(m - 1.0, m + 1.0);
+    const double ls = s * horner_c(c_LOGC, s * s);
+    const double ed = double(e);
+    return fma(ed, 0.69314718055994528623, fma(ed, 2.3190468138462996e-17, ls));
+#else
+    return log(x);
+#endif
+}
+
+// sqrt(w), w >= 0 finite: rsqrt seed + two Newton steps + one residual correction.
+__device__ __forceinline__ double sqrt_fast(double w) {
+#if CFUST_OWN_ELEM
+    double y;
+    asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(w));
+    y = y * fma(-0.5 * w * y, y, 1.5);
+    y = y * fma(-0.5 * w * y, y, 1.5);
+    double v = w * y;
+    v = fma(0.5 * y, fma(-v, v, w), v);
+    return (w > 0.0) ? v : 0.0;
+#else
+    return sqrt(w);
+#endif
+}
+
 // Phi(x) = P(X <= x), X ~ N(0,1); relative accuracy in the lower tail (to ~1e-307), absolute
 // accuracy for x > 0.  x^2 is split exactly (hi + lo) so the exponent carries no rounding.
 __device__ __forceinline__ double Phi_fast(double x) {
-    const double ax = fmin(fabs(x), 40.0);   // exp(-800) = 0: Phi is exactly 0 or 1 beyond
+    const double fx = fabs(x);
+    const double ax = (fx < 40.0) ? fx : 40.0;   // exp(-800) = 0: Phi is exactly 0 or 1 beyond
     const double hi = ax * ax;
     const double lo = fma(ax, ax, -hi);
-    const double e = exp(-0.5 * hi) * (1.0 - 0.5 * lo);
+    const double e = exp_neg(-0.5 * hi) * (1.0 - 0.5 * lo);
 #if CFUST_HORNER
     const double t = e * div_fast(horner_c(c_PH_P, ax), horner_c(c_PH_Q, ax));
 #else
@@ -75,9 +132,10 @@ __device__ __forceinline__ double Phi_fast(double x) {
 // Phi^{-1}(u), 0 < u < 1.  1 - u is exact for u >= 1/2; 2t is exact; log(2t) is accurate to
 // ~1 ulp of its value, so w keeps full relative precision as u -> 1/2.
 __device__ __forceinline__ double Phiinv_fast(double u) {
-    const double t = fmin(u, 1.0 - u);
-    const double w = -log(2.0 * t);
-    const double v = sqrt(w);
+    const double uc = 1.0 - u;
+    const double t = (u < uc) ? u : uc;
+    const double w = -log_unit(2.0 * t);
+    const double v = sqrt_fast(w);
 #if CFUST_HORNER
     const double z = w * div_fast(horner_c(c_NI_P, v), horner_c(c_NI_Q, v));
 #else

@@ -27,7 +27,10 @@ __global__ void __launch_bounds__(256, MINB) sov_bench(const double* __restrict_
 #pragma unroll
             for (int k = 1; k < R; ++k) {
                 const double w = __ldg(W + k * M + l);
-                z[k - 1] = Phiinv(fmin(fmax(w * e, UMIN), UMAX));
+                double u = w * e;
+            u = (u < UMIN) ? UMIN : u;
+            u = (u > UMAX) ? UMAX : u;
+            z[k - 1] = Phiinv(u);
                 double a = s * binv[k];
 #pragma unroll
                 for (int t = 0; t < k; ++t) a -= Cn[(k * (k - 1)) / 2 + t] * z[t];
@@ -88,5 +91,7 @@ int upload_special_constants_tool() {
     cudaMemcpyToSymbol(c_PH_Q, h_PH_Q, sizeof(h_PH_Q));
     cudaMemcpyToSymbol(c_NI_P, h_NI_P, sizeof(h_NI_P));
     cudaMemcpyToSymbol(c_NI_Q, h_NI_Q, sizeof(h_NI_Q));
+    cudaMemcpyToSymbol(c_EXPC, h_EXPC, sizeof(h_EXPC));
+    cudaMemcpyToSymbol(c_LOGC, h_LOGC, sizeof(h_LOGC));
     return 0;
 }
