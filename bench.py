@@ -40,6 +40,9 @@ FP64_PEAK_NOMINAL_TFLOPS = 148 * 64 * 2 * 1.965e9 / 1e12
 # counters 2*dfma + dadd + dmul over one E-step launch at n=4000 (12000 pairs):
 # profiles/r01_ncu_estep_cfg2.txt.  Re-measured whenever the kernel changes.
 FP64_FLOPS_PER_PAIR = {2: 1.2090e7}
+# dram__bytes_read.sum + dram__bytes_write.sum of one full-size cfg2 E-step launch (n=1e5):
+# 9.06 MB + 6.22 MB (profiles/r01_ncu_estep_cfg2_full.txt).  Algorithmic bytes: y = 3.2 MB.
+TRAFFIC_BYTES_PER_LAUNCH = {2: 15.28e6}
 
 
 def env_rank():
@@ -268,7 +271,9 @@ def main():
     peak_meas = measure_fp64_peak()
     roof = {"bound": "alu", "unit": "TFLOP/s", "peak": FP64_PEAK_NOMINAL_TFLOPS,
             "peak_kind": "nominal FP64 (148 SM x 64 DFMA/clk x 2 x 1.965 GHz)",
-            "fp64_peak_measured_tflops": peak_meas, "traffic": None,
+            "fp64_peak_measured_tflops": peak_meas,
+            "traffic": TRAFFIC_BYTES_PER_LAUNCH.get(args.config) if args.n == 0 else None,
+            "traffic_unit": "bytes per E-step launch (ncu dram read+write)",
             "kernel": "estep_cfust_kernel", "kernel_ms": est_ms,
             "sov_evals_per_s": evals / (est_ms * 1e-3)}
     if fpp:

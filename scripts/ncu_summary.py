@@ -13,17 +13,19 @@ def run(args):
 
 def main(rep, pairs, out):
     raw = list(csv.reader(io.StringIO(run([rep, "--page", "raw", "--csv"]))))
-    hdr, vals = raw[0], raw[2]
+    hdr, units, vals = raw[0], raw[1], raw[2]
     d = dict(zip(hdr, vals))
+    unit = dict(zip(hdr, units))
     cyc = float(d["sm__cycles_elapsed.avg"])
     f = lambda k: float(d[k]) * cyc
     fma = f("smsp__sass_thread_inst_executed_op_dfma_pred_on.sum.per_cycle_elapsed")
     add = f("smsp__sass_thread_inst_executed_op_dadd_pred_on.sum.per_cycle_elapsed")
     mul = f("smsp__sass_thread_inst_executed_op_dmul_pred_on.sum.per_cycle_elapsed")
     flops = 2 * fma + add + mul
-    dur = float(d["gpu__time_duration.sum"]) * 1e-3
+    scale = {"ns": 1e-9, "us": 1e-6, "usecond": 1e-6, "ms": 1e-3, "msecond": 1e-3, "s": 1.0}
+    dur = float(d["gpu__time_duration.sum"]) * scale.get(unit.get("gpu__time_duration.sum", "ms"), 1e-3)
     lines = [f"report: {rep}", f"kernel: {vals[hdr.index('Kernel Name')] if 'Kernel Name' in hdr else '?'}",
-             f"duration_ms: {float(d['gpu__time_duration.sum']):.4f}   sm_cycles: {cyc:.0f}",
+             f"duration_ms: {dur * 1e3:.4f}   sm_cycles: {cyc:.0f}",
              f"fp64 executed flops (2*dfma+dadd+dmul): {flops:.4e}   per pair ({pairs} pairs): {flops / pairs:.4e}",
              f"fp64 achieved: {flops / dur / 1e12:.2f} TFLOP/s   flop fraction of 148x64x2/clk: {flops / cyc / 18944:.3f}"]
     for k in ["sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_elapsed",
@@ -32,7 +34,7 @@ def main(rep, pairs, out):
               "smsp__thread_inst_executed_per_inst_executed.ratio", "sm__warps_active.avg.per_cycle_active",
               "launch__registers_per_thread", "launch__grid_size", "launch__block_size",
               "dram__bytes_read.sum", "dram__bytes_write.sum", "l1tex__t_sectors_pipe_lsu_mem_local_op_ld.sum"]:
-        lines.append(f"{k}: {d.get(k)}")
+        lines.append(f"{k}: {d.get(k)} {unit.get(k, '')}")
     lines.append("stall reasons (warps per issue-active cycle):")
     for h, v in zip(hdr, vals):
         if "average_warps_issue_stalled" in h and h.endswith("ratio"):
