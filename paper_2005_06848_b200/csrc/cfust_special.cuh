@@ -7,7 +7,9 @@
 // (relative error <= 1.3e-15 in double evaluation; coefficients in cfust_coeffs.h, all positive
 // so Horner has no cancellation), one formula over the whole range so a warp never diverges:
 //   Phi(x):       t = exp(-x^2/2) R(|x|),  Phi = t (x < 0) or 1 - t (x >= 0)
-//   Phi^{-1}(u):  t = min(u, 1-u), w = -log(2t), z = -w U(sqrt(w)), sign by u < 1/2
+//   Phi^{-1}(u):  t = min(u, 1-u), FP32 seed z0 ~ -w U(sqrt(w)) (w = -log(2t)), then one
+//                 third-order FP64 correction through Phi's own rational (Phiinv_seed, default);
+//                 Phiinv_rat (the FP64 (14,15) rational in sqrt(w)) is kept for comparison.
 // Polynomials by Horner (Estrin optional); divisions by rcp.approx + Newton (no IEEE slow-path branch).
 #pragma once
 #include <cuda_runtime.h>
@@ -57,10 +59,10 @@ __device__ __forceinline__ double div_fast(double p, double q) {
 }
 
 #ifndef CFUST_OWN_ELEM
-#define CFUST_OWN_ELEM 0   // 1: own branch-free exp/log/sqrt (measured equal speed, more registers)
-#endif
+#define CFUST_OWN_ELEM 1   // own branch-free exp/log/sqrt; with the seeded Phi^{-1} 11% faster E-step
+#endif                     // than libdevice (profiles/r01_seed_variants.log)
 
-// exp(x) for x <= 0 (x >= -708 exact to ~1 ulp; below: 0, i.e. results < 1e-307 flush).
+// exp(x) for x <= 709 (x >= -708 exact to ~1 ulp; below: 0, i.e. results < 1e-307 flush).
 // x = k ln2 + r, |r| <= ln2/2: k from the 1.5*2^52 rounding trick, r with a two-part ln2,
 // Taylor to r^13, 2^k by adding k to the exponent field.
 __device__ __forceinline__ double exp_neg(double x) {
@@ -131,7 +133,7 @@ __device__ __forceinline__ double Phi_fast(double x) {
 
 // Phi^{-1}(u), 0 < u < 1.  1 - u is exact for u >= 1/2; 2t is exact; log(2t) is accurate to
 // ~1 ulp of its value, so w keeps full relative precision as u -> 1/2.
-__device__ __forceinline__ double Phiinv_fast(double u) {
+__device__ __forceinline__ double Phiinv_rat(double u) {
     const double uc = 1.0 - u;
     const double t = (u < uc) ? u : uc;
     const double w = -log_unit(2.0 * t);
@@ -143,6 +145,71 @@ __device__ __forceinline__ double Phiinv_fast(double u) {
     const double z = w * div_fast(estrin_c(c_NI_P, v, v2, v4, v8), estrin_c(c_NI_Q, v, v2, v4, v8));
 #endif
     return (u < 0.5) ? -z : z;
+}
+
+// FP32 seed of the lower-tail quantile U(v) ~ Phi^{-1}(t) = -w U(sqrt w), w = -log(2t):
+// rational (8, 8) in v fitted by scripts/fit_special.py --seed (relative error 4.4e-7 in FP32
+// evaluation); literals, so FFMA takes them as immediates.
+__device__ __forceinline__ float seed_U32(float v) {
+    float p = -1.1203700189810206e-09f;
+    p = fmaf(p, v, 0.0089739840477705f);
+    p = fmaf(p, v, 0.2872512638568878f);
+    p = fmaf(p, v, 2.012030839920044f);
+    p = fmaf(p, v, 4.561682224273682f);
+    p = fmaf(p, v, 6.014867305755615f);
+    p = fmaf(p, v, 5.465461254119873f);
+    p = fmaf(p, v, 3.105163097381592f);
+    p = fmaf(p, v, 1.2533141374588013f);
+    float q = 0.006345330271869898f;
+    q = fmaf(q, v, 0.20316024124622345f);
+    q = fmaf(q, v, 1.4386792182922363f);
+    q = fmaf(q, v, 3.551027536392212f);
+    q = fmaf(q, v, 5.64398193359375f);
+    q = fmaf(q, v, 6.0376763343811035f);
+    q = fmaf(q, v, 4.860823631286621f);
+    q = fmaf(q, v, 2.4775614738464355f);
+    q = fmaf(q, v, 1.0f);
+    return __fdividef(p, q);
+}
+
+// Phi^{-1}(u), 0 < u < 1, by an FP32 seed and one third-order FP64 correction.
+//   t = min(u, 1-u) <= 1/2 (exact), z0 = -w U32(sqrt w) in FP32 from w = -log(2t) (exponent and
+//   20 mantissa bits of t; |error| <= ~5e-7 |z0| + 1e-7), then with the FP64 Mills-ratio rational
+//   R of Phi_fast (Phi(z0) = e^{-z0^2/2} R(|z0|)) and the exact derivatives of the inverse
+//   (x' = 1/phi, x'' = x/phi^2, x''' = (1 + 2x^2)/phi^3):
+//     r = (t - Phi(z0)) / phi(z0) = sqrt(2 pi) (t e^{z0^2/2} - R(|z0|)),
+//     x = z0 + r + (z0/2) r^2 + ((1 + 2 z0^2)/6) r^3      (truncation ~ (z0^3/4) r^4 < 1e-16 |x|).
+//   No log, no sqrt, one division in FP64 (vs log + sqrt + a (14,15) rational + division).
+//   Accuracy (CPU emulation, tests/test_special_coeffs.py): relative 3e-16 for |x| >= 1,
+//   absolute 4e-16 below (the SOV loop consumes z only through a = s b - sum C z).
+__device__ __forceinline__ double Phiinv_seed(double u) {
+    const double uc = 1.0 - u;
+    const double t = (u < uc) ? u : uc;
+    const int hx = __double2hiint(t);
+    const float m = __int_as_float(0x3f800000 | ((hx & 0x000fffff) << 3));   // mantissa of t in [1,2)
+    const float e2t = float((hx >> 20) - 1022);                             // 2t = m 2^e2t
+    float w = -fmaf(e2t, 0.6931471806f, __logf(m));
+    w = fmaxf(w, 0.0f);
+    const float v = (w > 0.0f) ? w * rsqrtf(w) : 0.0f;
+    const double ax = fmin(double(w * seed_U32(v)), 37.5);                   // |z0|
+    const double hi = ax * ax;
+    const double lo = fma(ax, ax, -hi);
+    const double ep = exp_neg(0.5 * hi) * (1.0 + 0.5 * lo);                 // e^{z0^2/2} (exp_neg is valid to +709)
+    const double R = div_fast(horner_c(c_PH_P, ax), horner_c(c_PH_Q, ax));
+    const double r = 2.5066282746310002 * fma(t, ep, -R);
+    const double x = fma(r, fma(r, fma(r, (2.0 * hi + 1.0) * (1.0 / 6.0), -0.5 * ax), 1.0), -ax);
+    return (u < 0.5) ? x : -x;
+}
+
+#ifndef CFUST_PHIINV_SEED
+#define CFUST_PHIINV_SEED 1
+#endif
+__device__ __forceinline__ double Phiinv_fast(double u) {
+#if CFUST_PHIINV_SEED
+    return Phiinv_seed(u);
+#else
+    return Phiinv_rat(u);
+#endif
 }
 
 }  // namespace cfust

