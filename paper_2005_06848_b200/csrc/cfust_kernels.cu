@@ -52,16 +52,61 @@ struct WarpScratch {
 // SOV point loop for T_R (chi-normal form, reading R-T): this lane's share of
 //   sum_l prod_k Phi(a_k(l)),  a_0 = s_l binv_0,  a_k = s_l binv_k - sum_{t<k} Cn_kt z_t,
 //   z_t = Phi^{-1}(clamp(w_{l,t+1} e_t)).
-#ifndef CFUST_NPTS
-#define CFUST_NPTS 1
+// Per-q tuning of estep_cfust_kernel<Q> (measured on B200, profiles/r01_tuning.log):
+//   NP   lattice points per lane per loop iteration (independent SOV chains for the FP64 pipe),
+//   MB   resident blocks per SM the register budget must allow (__launch_bounds__).
+// CFUST_NP_Q<q> / CFUST_MB_Q<q> override them for experiment builds (scripts/build_variants.py).
+#ifndef CFUST_NP_Q1
+#define CFUST_NP_Q1 1
 #endif
-constexpr int NPTS = CFUST_NPTS;   // lattice points per lane per iteration (independent chains)
+#ifndef CFUST_NP_Q2
+#define CFUST_NP_Q2 1
+#endif
+#ifndef CFUST_NP_Q3
+#define CFUST_NP_Q3 1
+#endif
+#ifndef CFUST_NP_Q4
+#define CFUST_NP_Q4 2
+#endif
+#ifndef CFUST_NP_Q5
+#define CFUST_NP_Q5 2
+#endif
+#ifndef CFUST_NP_Q6
+#define CFUST_NP_Q6 2
+#endif
+#ifndef CFUST_MB_Q1
+#define CFUST_MB_Q1 CFUST_MINB
+#endif
+#ifndef CFUST_MB_Q2
+#define CFUST_MB_Q2 CFUST_MINB
+#endif
+#ifndef CFUST_MB_Q3
+#define CFUST_MB_Q3 CFUST_MINB
+#endif
+#ifndef CFUST_MB_Q4
+#define CFUST_MB_Q4 1
+#endif
+#ifndef CFUST_MB_Q5
+#define CFUST_MB_Q5 1
+#endif
+#ifndef CFUST_MB_Q6
+#define CFUST_MB_Q6 1
+#endif
+template <int Q>
+struct Tune {
+    static constexpr int NP = Q == 1 ? CFUST_NP_Q1 : Q == 2 ? CFUST_NP_Q2 : Q == 3 ? CFUST_NP_Q3
+                            : Q == 4 ? CFUST_NP_Q4 : Q == 5 ? CFUST_NP_Q5 : CFUST_NP_Q6;
+    static constexpr int MB = Q == 1 ? CFUST_MB_Q1 : Q == 2 ? CFUST_MB_Q2 : Q == 3 ? CFUST_MB_Q3
+                              : Q == 4 ? CFUST_MB_Q4 : Q == 5 ? CFUST_MB_Q5 : CFUST_MB_Q6;
+};
 
-template <int R>
+template <int R, int NPTS>
 __device__ __forceinline__ double sov_lane_sum(const double (&binv)[R], const double (&Cn)[R * (R - 1) / 2],
                                                const double *__restrict__ chi, const double *__restrict__ W, int M,
                                                int lane) {
-    // NPTS lattice points per iteration (l, l + 32, ...): independent chains for the FP64 pipe
+    // NPTS lattice points per iteration (l, l + 32, ...): independent chains for the FP64 pipe.
+    // M is a power of two >= 1024, so 32 * NPTS divides it exactly when NPTS is a power of two.
+    static_assert(NPTS == 1 || NPTS == 2 || NPTS == 4, "NPTS must divide M / 32");
     double acc[NPTS];
 #pragma unroll
     for (int j = 0; j < NPTS; ++j) acc[j] = 0.0;
@@ -100,7 +145,7 @@ __device__ __forceinline__ double sov_lane_sum(const double (&binv)[R], const do
 
 // T_R(b; 0, S, m): R = 0 -> 1; R = 1 -> univariate t CDF; R >= 2 -> lattice rule with
 // univariate-prioritisation reordering (ascending b_k / sqrt(S_kk), stable; reading A13).
-template <int R>
+template <int R, int NP>
 __device__ __noinline__ double T_eval(const double *b, const double *S, int lds, double m,
                                       const double *__restrict__ chi, const double *__restrict__ W, int M,
                                       int lane) {
@@ -138,7 +183,7 @@ __device__ __noinline__ double T_eval(const double *b, const double *S, int lds,
         for (int k = 1; k < R; ++k)
 #pragma unroll
             for (int t = 0; t < k; ++t) Cn[(k * (k - 1)) / 2 + t] = C[k][t] / C[k][k];
-        const double acc = sov_lane_sum<R>(binv, Cn, chi, W, M, lane);
+        const double acc = sov_lane_sum<R, NP>(binv, Cn, chi, W, M, lane);
         return warp_sum(acc) / double(M);
     }
 }
@@ -176,7 +221,7 @@ __device__ void pair_eval(const CompDev &cp, int p, const double *__restrict__ W
     const double sq0 = sqrt(m0 / rho);
 #pragma unroll
     for (int k = 0; k < Q; ++k) ws.b[k] = c[k] * sq0;
-    const double T0 = T_eval<Q>(ws.b, cp.Lam, QMAX, m0, chi, W, M, lane);
+    const double T0 = T_eval<Q, Tune<Q>::NP>(ws.b, cp.Lam, QMAX, m0, chi, W, M, lane);
     if (MODE == 1) {
         res[0] = (T0 > 0.0) ? Q * CUDART_LN2 + logt + log(T0) : -CUDART_INF;
         return;
@@ -184,7 +229,7 @@ __device__ void pair_eval(const CompDev &cp, int p, const double *__restrict__ W
     const double sq2 = sqrt((m0 + 2.0) / rho);
 #pragma unroll
     for (int k = 0; k < Q; ++k) ws.b[k] = c[k] * sq2;
-    const double T2 = T_eval<Q>(ws.b, cp.Lam, QMAX, m0 + 2.0, chi + 2 * M, W, M, lane);
+    const double T2 = T_eval<Q, Tune<Q>::NP>(ws.b, cp.Lam, QMAX, m0 + 2.0, chi + 2 * M, W, M, lane);
     res[1] = cp.psi_half_m0 - log(0.5 * rho) - m0 / rho;      // e1 - e2, reading A5
     if (!(T0 > 0.0)) {                                          // reading A16
         res[0] = -CUDART_INF;
@@ -244,7 +289,7 @@ __device__ void pair_eval(const CompDev &cp, int p, const double *__restrict__ W
                     }
                     ++ib;
                 }
-                const double val = T_eval<Q2>(ws.bc, ws.Sc, QMAX, m0, chi, W, M, lane);
+                const double val = T_eval<Q2, Tune<Q>::NP>(ws.bc, ws.Sc, QMAX, m0, chi, W, M, lane);
                 ws.Tkt[k * QMAX + t] = val;
                 ws.Tkt[t * QMAX + k] = val;            // symmetric in {k, t} (A17)
             }
@@ -254,7 +299,7 @@ __device__ void pair_eval(const CompDev &cp, int p, const double *__restrict__ W
 #pragma unroll
     for (int k = 0; k < Q; ++k) {
         double tk = 1.0;
-        if constexpr (Q >= 2) tk = T_eval<Q1>(ws.ct[k], ws.St[k], QMAX, m0 + 1.0, chi + M, W, M, lane);
+        if constexpr (Q >= 2) tk = T_eval<Q1, Tune<Q>::NP>(ws.ct[k], ws.St[k], QMAX, m0 + 1.0, chi + M, W, M, lane);
         ws.Tk[k] = tk;
         h[k] = ws.phi[k] * tk;
     }
@@ -356,7 +401,7 @@ struct EArgs {
 
 // MODE 0: E-step statistics; 1: log-likelihood only; 2: per-pair dump of idx[0..cnt).
 template <int Q, int MODE>
-__global__ void __launch_bounds__(EW * 32, MINB) estep_cfust_kernel(EArgs A) {
+__global__ void __launch_bounds__(EW * 32, Tune<Q>::MB) estep_cfust_kernel(EArgs A) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const int p = A.p, g = A.g, K = A.K, GK = g * K;

@@ -147,6 +147,24 @@ __device__ __forceinline__ double Phiinv_rat(double u) {
     return (u < 0.5) ? -z : z;
 }
 
+// FP32 MUFU approximations with flush-to-zero (no subnormal pre-scaling instructions; the
+// arguments here are never subnormal).
+__device__ __forceinline__ float lg2_ftz(float x) {
+    float r;
+    asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
+__device__ __forceinline__ float rsqrt_ftz(float x) {
+    float r;
+    asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
+__device__ __forceinline__ float rcp_ftz(float x) {
+    float r;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
+
 // FP32 seed of the lower-tail quantile U(v) ~ Phi^{-1}(t) = -w U(sqrt w), w = -log(2t):
 // rational (8, 8) in v fitted by scripts/fit_special.py --seed (relative error 4.4e-7 in FP32
 // evaluation); literals, so FFMA takes them as immediates.
@@ -169,7 +187,7 @@ __device__ __forceinline__ float seed_U32(float v) {
     q = fmaf(q, v, 4.860823631286621f);
     q = fmaf(q, v, 2.4775614738464355f);
     q = fmaf(q, v, 1.0f);
-    return __fdividef(p, q);
+    return p * rcp_ftz(q);
 }
 
 // Phi^{-1}(u), 0 < u < 1, by an FP32 seed and one third-order FP64 correction.
@@ -188,9 +206,9 @@ __device__ __forceinline__ double Phiinv_seed(double u) {
     const int hx = __double2hiint(t);
     const float m = __int_as_float(0x3f800000 | ((hx & 0x000fffff) << 3));   // mantissa of t in [1,2)
     const float e2t = float((hx >> 20) - 1022);                             // 2t = m 2^e2t
-    float w = -fmaf(e2t, 0.6931471806f, __logf(m));
+    float w = -0.6931471806f * (e2t + lg2_ftz(m));
     w = fmaxf(w, 0.0f);
-    const float v = (w > 0.0f) ? w * rsqrtf(w) : 0.0f;
+    const float v = (w > 0.0f) ? w * rsqrt_ftz(w) : 0.0f;
     const double ax = fmin(double(w * seed_U32(v)), 37.5);                   // |z0|
     const double hi = ax * ax;
     const double lo = fma(ax, ax, -hi);
