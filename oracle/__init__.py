@@ -64,21 +64,25 @@ def lib():
         L.orc_chi_table.argtypes = [C.POINTER(_Lattice), _D, _PD]
         L.orc_Tr.restype = _D
         L.orc_Tr.argtypes = [_I, _PD, _PD, _D, C.POINTER(_Lattice), _PD, _PD]
+        L.orc_Tr_w.restype = _D
+        L.orc_Tr_w.argtypes = [_I, _PD, _PD, _D, C.POINTER(_Lattice), _PD, _PD, _PD, _PD]
+        L.orc_logchi_table.restype = None
+        L.orc_logchi_table.argtypes = [C.POINTER(_Lattice), _D, _PD]
         L.orc_derive.restype = _I
         L.orc_derive.argtypes = [_I, _I, _PD, _PD, _D, _PD, _PD, _PD, _PD, _PD]
         L.orc_pair.restype = _I
         L.orc_pair.argtypes = [_I, _I, _PD, _PD, _PD, _PD, _PD, _D, _D, C.POINTER(_Lattice),
-                               _PD, _PD, _PD, _PD, _PD]
+                               _PD, _PD, _PD, _PD, _PD, _PD]
         L.orc_estep.restype = _I
         L.orc_estep.argtypes = [_I64, _I, _I, _I, _PD, _PD, _PD, _PD, _PD, _PD, C.POINTER(_Lattice),
-                                _I, _PD, _PD, _PD, _PD]
+                                _I, _I, _PD, _PD, _PD, _PD]
         L.orc_mstep.restype = _I
         L.orc_mstep.argtypes = [_I, _I, _I, _D, _PD, _PD, _PD, _PD, _PD, _PD, _D, _D]
         L.orc_aitken_stop.restype = _I
         L.orc_aitken_stop.argtypes = [_D, _D, _D, _D]
         L.orc_fit.restype = _I
         L.orc_fit.argtypes = [_I64, _I, _I, _I, _PD, _PD, _PD, _PD, _PD, _PD, C.POINTER(_Lattice),
-                              _I, _I, _D, _D, _D, _PD, C.POINTER(_I), C.POINTER(_I)]
+                              _I, _I, _I, _D, _D, _D, _PD, C.POINTER(_I), C.POINTER(_I)]
         L.orc_k_stats.restype = _I
         L.orc_k_stats.argtypes = [_I, _I]
     return _lib
@@ -135,6 +139,12 @@ def chi_table(lat: Lattice, m: float) -> np.ndarray:
     return out
 
 
+def logchi_table(lat: Lattice, m: float) -> np.ndarray:
+    out = np.empty(lat.M)
+    lib().orc_logchi_table(lat.ptr, float(m), _p(out))
+    return out
+
+
 def Tr(b, S, m, lat: Lattice | None = None, chi_s: np.ndarray | None = None, return_gap=False):
     """T_r(b; 0, S, m) by the chi-normal SOV on the lattice (r = len(b))."""
     b = _f64(b).ravel()
@@ -163,21 +173,24 @@ def derive(sigma, delta, nu):
     return rc, {"L": L, "A": A[:q], "Lambda": Lam[:q, :q], "logdet": ld[0], "kappa": ka[0]}
 
 
-def pair(y, mu, sigma, delta, nu, lat: Lattice | None):
-    """One (observation, component) pair: dict(logf_noprior, e1me2, e2, e3, e4)."""
+def pair(y, mu, sigma, delta, nu, lat: Lattice | None, e1_exact: bool = False):
+    """One (observation, component) pair: dict(logf_noprior, e1me2, e2, e3, e4).
+    e1_exact: e1 = E[log W | y] on T0's lattice points (reading R2') instead of reading A5."""
     y = _f64(y); mu = _f64(mu); p = len(y)
     delta = _f64(delta).reshape(p, -1); q = delta.shape[1]
     rc, dv = derive(sigma, delta, nu)
     assert rc == OK, rc
     m0 = nu + p
-    tabs = [chi_table(lat, m0 + k) if (lat is not None and q >= 2) else np.zeros(1) for k in range(3)]
+    use_lat = lat is not None and (q >= 2 or (e1_exact and q >= 1))
+    tabs = [chi_table(lat, m0 + k) if use_lat else np.zeros(1) for k in range(3)]
+    lv = logchi_table(lat, m0) if (e1_exact and q >= 1) else None
     out = np.zeros(3 + q + q * q)
     gap = np.array([np.inf])
     A = _f64(dv["A"]) if q else np.zeros(1)
     Lam = _f64(dv["Lambda"]) if q else np.zeros(1)
     rc = lib().orc_pair(p, q, _p(y), _p(mu), _p(dv["L"]), _p(A), _p(Lam), float(nu), float(dv["kappa"]),
                         lat.ptr if lat is not None else None, _p(tabs[0]), _p(tabs[1]), _p(tabs[2]),
-                        _p(out), _p(gap))
+                        _p(lv) if lv is not None else None, _p(out), _p(gap))
     assert rc == OK, rc
     return {"logf": out[0], "e1me2": out[1], "e2": out[2], "e3": out[3:3 + q],
             "e4": out[3 + q:].reshape(q, q), "gap": gap[0]}
@@ -190,7 +203,8 @@ def _params(params: dict, g: int, p: int, q: int):
             _f64(params["nu"]).reshape(g))
 
 
-def estep(y, params: dict, q: int, lat: Lattice | None, nthreads=None, pairs=False, gaps=False):
+def estep(y, params: dict, q: int, lat: Lattice | None, nthreads=None, pairs=False, gaps=False,
+          e1_exact: bool = False):
     """Full E-step.  Returns dict(stats [g*K+1], loglik, pairs [n,g,4+q+q*q] optional)."""
     y = _f64(y)
     n, p = y.shape
@@ -202,7 +216,7 @@ def estep(y, params: dict, q: int, lat: Lattice | None, nthreads=None, pairs=Fal
     po = np.zeros((n, g, 4 + q + q * q)) if pairs else None
     gp = np.full((n, g), np.inf) if gaps else None
     rc = lib().orc_estep(n, p, q, g, _p(y), _p(pi), _p(mu), _p(sg), _p(de), _p(nu),
-                         lat.ptr if lat is not None else None, _nt(nthreads),
+                         lat.ptr if lat is not None else None, _nt(nthreads), int(bool(e1_exact)),
                          _p(po) if pairs else None, _p(stats), _p(ll), _p(gp) if gaps else None)
     out = {"rc": rc, "stats": stats, "loglik": ll[0]}
     if pairs:
@@ -224,7 +238,7 @@ def mstep(stats, params: dict, p: int, q: int, n_total: float, nu_lo=0.1, nu_hi=
 
 
 def fit(y, params: dict, q: int, lat: Lattice | None, max_iter: int, tol: float = 0.0,
-        nthreads=None, nu_lo=0.1, nu_hi=1000.0):
+        nthreads=None, nu_lo=0.1, nu_hi=1000.0, e1_exact: bool = False):
     y = _f64(y)
     n, p = y.shape
     g = len(params["pi"])
@@ -232,7 +246,8 @@ def fit(y, params: dict, q: int, lat: Lattice | None, max_iter: int, tol: float 
     trace = np.zeros(max_iter + 1)
     ni = C.c_int(0); cv = C.c_int(0)
     rc = lib().orc_fit(n, p, q, g, _p(y), _p(pi), _p(mu), _p(sg), _p(de), _p(nu),
-                       lat.ptr if lat is not None else None, _nt(nthreads), int(max_iter), float(tol),
+                       lat.ptr if lat is not None else None, _nt(nthreads), int(bool(e1_exact)), int(max_iter),
+                       float(tol),
                        float(nu_lo), float(nu_hi), _p(trace), C.byref(ni), C.byref(cv))
     params_out = {"pi": pi, "mu": mu, "sigma": sg,
                   "delta": de.reshape(g, p, q) if q > 0 else np.zeros((g, p, 0)), "nu": nu}

@@ -259,6 +259,11 @@ void orc_chi_table(const orc_lattice *L, double m, double *s_out) {
     for (int64_t l = 0; l < L->M; ++l) s_out[l] = sqrt(orc_chi2_quantile(orc_lattice_w(L, l, 0), m) / m);
 }
 
+/* log V_l = log chi2_m^{-1}(w_{l,0}): the log of the chi-square node behind s_l (exact e1, R2'). */
+void orc_logchi_table(const orc_lattice *L, double m, double *out) {
+    for (int64_t l = 0; l < L->M; ++l) out[l] = log(orc_chi2_quantile(orc_lattice_w(L, l, 0), m));
+}
+
 /* =====================================================================================
  * T_r(b; 0, S, m) — Genz-Bretz separation of variables for the multivariate t in its
  * chi-normal form (reading R-T):  T_r(b;S,m) = E_V[ Phi_r( b sqrt(V/m); S ) ],
@@ -266,9 +271,22 @@ void orc_chi_table(const orc_lattice *L, double m, double *s_out) {
  * Variables are reordered by ascending b_k/sqrt(S_kk), stable (reading A13/A14).
  * r = 0 -> 1;  r = 1 -> closed form T_m(b/sqrt(S)).
  * ===================================================================================== */
-double orc_Tr(int r, const double *b, const double *S, double m, const orc_lattice *L,
-              const double *chi_s, double *min_key_gap) {
+/* With lv != NULL (exact e1, reading R2'): also *wsum = (1/M) sum_l f_l lv_l over the same
+ * lattice points, and r = 1 is evaluated on the lattice too (f_l = Phi(s_l b / sqrt(S))). */
+static double tr_core(int r, const double *b, const double *S, double m, const orc_lattice *L,
+                      const double *chi_s, const double *lv, double *min_key_gap, double *wsum) {
     if (r == 0) return 1.0;
+    if (r == 1 && lv) {
+        double sum = 0.0, ws = 0.0;
+        const double bs = b[0] / sqrt(S[0]);
+        for (int64_t l = 0; l < L->M; ++l) {
+            const double f = orc_norm_cdf(chi_s[l] * bs);
+            sum += f;
+            ws += f * lv[l];
+        }
+        *wsum = ws / (double)L->M;
+        return sum / (double)L->M;
+    }
     if (r == 1) return orc_t_cdf(b[0] / sqrt(S[0]), m);
     int perm[QMAX];
     double key[QMAX];
@@ -292,7 +310,7 @@ double orc_Tr(int r, const double *b, const double *S, double m, const orc_latti
         for (int j = 0; j < r; ++j) Sp[i * r + j] = S[perm[i] * r + perm[j]];
     }
     if (chol(r, Sp, C) != ORC_OK) return NAN;
-    double sum = 0.0;
+    double sum = 0.0, ws = 0.0;
     for (int64_t l = 0; l < L->M; ++l) {
         const double s = chi_s[l];
         double e = orc_norm_cdf(s * bp[0] / C[0]);
@@ -309,8 +327,20 @@ double orc_Tr(int r, const double *b, const double *S, double m, const orc_latti
             f *= e;
         }
         sum += f;
+        if (lv) ws += f * lv[l];
     }
+    if (lv) *wsum = ws / (double)L->M;
     return sum / (double)L->M;
+}
+
+double orc_Tr(int r, const double *b, const double *S, double m, const orc_lattice *L,
+              const double *chi_s, double *min_key_gap) {
+    return tr_core(r, b, S, m, L, chi_s, NULL, min_key_gap, NULL);
+}
+
+double orc_Tr_w(int r, const double *b, const double *S, double m, const orc_lattice *L,
+                const double *chi_s, const double *lv, double *min_key_gap, double *wsum) {
+    return tr_core(r, b, S, m, L, chi_s, lv, min_key_gap, wsum);
 }
 
 /* =====================================================================================
@@ -357,11 +387,16 @@ int orc_derive(int p, int q, const double *sigma, const double *delta, double nu
 /* =====================================================================================
  * O2-O8: one (observation, component) pair.
  * out = [log(2^q t_p T0)  (no log pi),  e1-e2,  e2,  e3 (q),  e4 (q*q)]
+ * e1 = E[log W | y]: lv_m0 == NULL -> the closed-form approximation (reading A5, R1);
+ * lv_m0 = log chi2_{m0}^{-1} node table -> exact (reading R2'):  with V ~ chi2_{m0} and
+ * W = V / rho a posteriori weighted by Phi_q(c sqrt(V/rho); Lambda),
+ *   e1 = E_V[log(V/rho) Phi_q] / E_V[Phi_q] = (sum_l f_l log V_l) / (sum_l f_l) - log rho
+ * on T0's own lattice points (f_l the SOV integrand of T0).
  * ===================================================================================== */
 int orc_pair(int p, int q, const double *y, const double *mu, const double *L_omega,
              const double *A, const double *Lambda, double nu, double kappa,
              const orc_lattice *L, const double *chi_m0, const double *chi_m1,
-             const double *chi_m2, double *out, double *min_key_gap) {
+             const double *chi_m2, const double *lv_m0, double *out, double *min_key_gap) {
     double r[PMAX], v[PMAX];
     for (int a = 0; a < p; ++a) r[a] = y[a] - mu[a];
     for (int a = 0; a < p; ++a) {          /* forward solve L v = r; d = |v|^2 */
@@ -389,7 +424,16 @@ int orc_pair(int p, int q, const double *y, const double *mu, const double *L_om
     /* T0 for the density (Eq. (2)), T2 for e2 */
     double bq[QMAX];
     for (int k = 0; k < q; ++k) bq[k] = c[k] * sqrt(m0 / rho);
-    const double T0 = orc_Tr(q, bq, Lambda, m0, L, chi_m0, min_key_gap);
+    double e1_exact = 0.0;
+    double T0;
+    if (lv_m0) {
+        double wsum = 0.0;
+        const double T0lat = orc_Tr_w(q, bq, Lambda, m0, L, chi_m0, lv_m0, min_key_gap, &wsum);
+        T0 = (q == 1) ? orc_Tr(1, bq, Lambda, m0, L, chi_m0, NULL) : T0lat;   /* density: exact T_1 */
+        e1_exact = wsum / T0lat - log(rho);
+    } else {
+        T0 = orc_Tr(q, bq, Lambda, m0, L, chi_m0, min_key_gap);
+    }
     for (int k = 0; k < q; ++k) bq[k] = c[k] * sqrt((m0 + 2.0) / rho);
     const double T2 = orc_Tr(q, bq, Lambda, m0 + 2.0, L, chi_m2, min_key_gap);
     const int PW = 3 + q + q * q;
@@ -491,6 +535,7 @@ int orc_pair(int p, int q, const double *y, const double *mu, const double *L_om
     const double fac = m0 / rho;
     out[0] = q * log(2.0) + logt + log(T0);
     out[2] = fac * T2 / T0;
+    if (lv_m0) out[1] = e1_exact - out[2];
     for (int a = 0; a < q; ++a) out[3 + a] = fac * E1[a] / T0;
     for (int a = 0; a < q; ++a)
         for (int b = 0; b < q; ++b)
@@ -504,17 +549,18 @@ int orc_pair(int p, int q, const double *y, const double *mu, const double *L_om
  * ===================================================================================== */
 typedef struct {
     double L[PMAX * PMAX], A[QMAX * PMAX], Lam[QMAX * QMAX], logdet, kappa;
-    double *chi0, *chi1, *chi2;
+    double *chi0, *chi1, *chi2, *lv0;
 } comp_derived;
 
 int orc_estep(int64_t n, int p, int q, int g, const double *y,
               const double *pi, const double *mu, const double *sigma,
               const double *delta, const double *nu, const orc_lattice *L,
-              int nthreads, double *pair_out, double *stats, double *loglik,
+              int nthreads, int e1_exact, double *pair_out, double *stats, double *loglik,
               double *min_key_gap) {
     if (p < 1 || p > PMAX || q < 0 || q > 6 || g < 1 || n < 0) return ORC_EINVAL;
-    const int need_lattice = q >= 2;
-    if (need_lattice && (L == NULL || L->s < q)) return ORC_EINVAL;
+    const int use_e1 = e1_exact && q >= 1;          /* q = 0: R1 is already exact */
+    const int need_lattice = q >= 2 || use_e1;
+    if (need_lattice && (L == NULL || L->M < 1 || L->s < (q > 1 ? q : 1))) return ORC_EINVAL;
     comp_derived *cd = (comp_derived *)calloc(g, sizeof(comp_derived));
     int rc = ORC_OK;
     for (int i = 0; i < g && rc == ORC_OK; ++i) {
@@ -528,6 +574,10 @@ int orc_estep(int64_t n, int p, int q, int g, const double *y,
             orc_chi_table(L, m0, cd[i].chi0);
             orc_chi_table(L, m0 + 1.0, cd[i].chi1);
             orc_chi_table(L, m0 + 2.0, cd[i].chi2);
+            if (use_e1) {
+                cd[i].lv0 = (double *)malloc(sizeof(double) * L->M);
+                orc_logchi_table(L, m0, cd[i].lv0);
+            }
         }
     }
     const int PW = 3 + q + q * q;        /* orc_pair output width */
@@ -549,7 +599,7 @@ int orc_estep(int64_t n, int p, int q, int g, const double *y,
             double gap = INFINITY;
             const int r2 = orc_pair(p, q, y + (size_t)j * p, mu + (size_t)i * p, cd[i].L, cd[i].A,
                                     cd[i].Lam, nu[i], cd[i].kappa, L, cd[i].chi0, cd[i].chi1,
-                                    cd[i].chi2, buf + (size_t)jj * PW, &gap);
+                                    cd[i].chi2, cd[i].lv0, buf + (size_t)jj * PW, &gap);
             gaps[jj] = gap;
             if (r2 != ORC_OK) prc = r2;
         }
@@ -601,7 +651,7 @@ int orc_estep(int64_t n, int p, int q, int g, const double *y,
     if (loglik) *loglik = ll;
     free(buf);
     free(gaps);
-    for (int i = 0; i < g; ++i) { free(cd[i].chi0); free(cd[i].chi1); free(cd[i].chi2); }
+    for (int i = 0; i < g; ++i) { free(cd[i].chi0); free(cd[i].chi1); free(cd[i].chi2); free(cd[i].lv0); }
     free(cd);
     return rc;
 }
@@ -713,17 +763,17 @@ int orc_aitken_stop(double l_km2, double l_km1, double l_k, double tol) {
 /* O13: E-step at Psi^(0) gives l^(0); then [M-step, E-step] per iteration. */
 int orc_fit(int64_t n, int p, int q, int g, const double *y, double *pi, double *mu,
             double *sigma, double *delta, double *nu, const orc_lattice *L,
-            int nthreads, int max_iter, double tol, double nu_lo, double nu_hi,
+            int nthreads, int e1_exact, int max_iter, double tol, double nu_lo, double nu_hi,
             double *trace, int *n_iter, int *converged) {
     const int K = orc_k_stats(p, q);
     double *stats = (double *)malloc(sizeof(double) * ((size_t)g * K + 1));
     *n_iter = 0;
     *converged = 0;
-    int rc = orc_estep(n, p, q, g, y, pi, mu, sigma, delta, nu, L, nthreads, NULL, stats, &trace[0], NULL);
+    int rc = orc_estep(n, p, q, g, y, pi, mu, sigma, delta, nu, L, nthreads, e1_exact, NULL, stats, &trace[0], NULL);
     for (int k = 1; k <= max_iter && rc == ORC_OK; ++k) {
         rc = orc_mstep(p, q, g, (double)n, stats, pi, mu, sigma, delta, nu, nu_lo, nu_hi);
         if (rc != ORC_OK) break;
-        rc = orc_estep(n, p, q, g, y, pi, mu, sigma, delta, nu, L, nthreads, NULL, stats, &trace[k], NULL);
+        rc = orc_estep(n, p, q, g, y, pi, mu, sigma, delta, nu, L, nthreads, e1_exact, NULL, stats, &trace[k], NULL);
         if (rc != ORC_OK) break;
         *n_iter = k;
         if (tol > 0.0 && k >= 2 && orc_aitken_stop(trace[k - 2], trace[k - 1], trace[k], tol)) {

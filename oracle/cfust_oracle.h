@@ -45,28 +45,33 @@ double orc_digamma(double x);
 /* ---- lattice (O0) ---- */
 double orc_lattice_w(const orc_lattice *L, int64_t l, int k);
 void orc_chi_table(const orc_lattice *L, double m, double *s_out);
+void orc_logchi_table(const orc_lattice *L, double m, double *out);   /* log chi2_m^{-1}(w_{l,0}) */
 
 /* ---- T_r(b; 0, S, m) (O4, chi-normal SOV reading R-T) ---- */
 double orc_Tr(int r, const double *b, const double *S, double m,
               const orc_lattice *L, const double *chi_s, double *min_key_gap);
+/* the same lattice rule, also returning *wsum = (1/M) sum_l f_l lv_l (r = 1 on the lattice) */
+double orc_Tr_w(int r, const double *b, const double *S, double m, const orc_lattice *L,
+                const double *chi_s, const double *lv, double *min_key_gap, double *wsum);
 
 /* ---- per-component derived quantities (O1) ---- */
 int orc_derive(int p, int q, const double *sigma, const double *delta, double nu,
                double *L_omega, double *A, double *Lambda, double *logdet, double *kappa);
 
-/* ---- per pair E-step quantities (O2-O8). out = [logf_noprior, e1me2, e2, e3(q), e4(q*q)] ---- */
+/* ---- per pair E-step quantities (O2-O8). out = [logf_noprior, e1me2, e2, e3(q), e4(q*q)]
+ * lv_m0 (may be NULL): log chi2_{m0}^{-1} node table -> exact e1 = E[log W | y] (reading R2') ---- */
 int orc_pair(int p, int q, const double *y, const double *mu, const double *L_omega,
              const double *A, const double *Lambda, double nu, double kappa,
              const orc_lattice *L, const double *chi_m0, const double *chi_m1,
-             const double *chi_m2, double *out, double *min_key_gap);
+             const double *chi_m2, const double *lv_m0, double *out, double *min_key_gap);
 
-/* ---- E-step over n observations (O9-O10) ----
+/* ---- E-step over n observations (O9-O10); e1_exact: 0 reading A5 (R1), 1 exact (R2') ----
  * pair_out (may be NULL): [n][g][4+q+q*q] = logf, tau, e1me2, e2, e3(q), e4(q*q)
  * stats (may be NULL): [g*K + 1], K = 3+p+p(p+1)/2+q+q(q+1)/2+p*q, last entry = loglik */
 int orc_estep(int64_t n, int p, int q, int g, const double *y,
               const double *pi, const double *mu, const double *sigma,
               const double *delta, const double *nu, const orc_lattice *L,
-              int nthreads, double *pair_out, double *stats, double *loglik,
+              int nthreads, int e1_exact, double *pair_out, double *stats, double *loglik,
               double *min_key_gap);
 
 /* ---- M-step (O11-O12), in place on the parameter arrays ---- */
@@ -80,7 +85,7 @@ int orc_aitken_stop(double l_km2, double l_km1, double l_k, double tol);
 /* ---- fit loop (O13): trace gets loglik^(0..n_iter) ---- */
 int orc_fit(int64_t n, int p, int q, int g, const double *y, double *pi, double *mu,
             double *sigma, double *delta, double *nu, const orc_lattice *L,
-            int nthreads, int max_iter, double tol, double nu_lo, double nu_hi,
+            int nthreads, int e1_exact, int max_iter, double tol, double nu_lo, double nu_hi,
             double *trace, int *n_iter, int *converged);
 
 int orc_k_stats(int p, int q);

@@ -239,3 +239,103 @@ def test_underflow_error(orc):
 def test_not_pd_error(orc):
     rc, _ = orc.derive(np.array([[1.0, 2.0], [2.0, 1.0]]), np.zeros((2, 1)), 5.0)
     assert rc == orc.ENOTPD
+
+
+# ------------------------------------------------------------------------------ exact e1 (R2')
+def _joint_grid_q1(p, mu, Sig, D, nu, y):
+    """2-D quadrature of the generative joint at q = 1: returns f, E[W|y], E[log W|y]."""
+    Si = np.linalg.inv(Sig)
+    ld = np.linalg.slogdet(Sig)[1]
+    xg, wg = np.polynomial.legendre.leggauss(40)
+
+    def grid(lo, hi, panels):
+        e = np.linspace(lo, hi, panels + 1)
+        x = ((e[1:, None] - e[:-1, None]) * (xg[None, :] + 1) / 2 + e[:-1, None]).ravel()
+        w = ((e[1:, None] - e[:-1, None]) / 2 * wg[None, :]).ravel()
+        return x, w
+    s_, ws = grid(-25.0, 6.0, 40)
+    v_, wv = grid(-40.0, 4.0, 40)
+    W, U = np.exp(s_)[:, None], np.exp(v_)[None, :]
+    jac = (ws * np.exp(s_))[:, None] * (wv * np.exp(v_))[None, :]
+    r0 = y - mu
+    a0, a1, a2 = r0 @ Si @ r0, D[:, 0] @ Si @ r0, D[:, 0] @ Si @ D[:, 0]
+    qf = a0 - 2 * a1 * U + a2 * U * U
+    ly = -0.5 * p * math.log(2 * math.pi) - 0.5 * ld + 0.5 * p * np.log(W) - 0.5 * W * qf
+    joint = st.gamma.pdf(W, nu / 2, scale=2 / nu) * 2 * st.norm.pdf(U, 0, 1 / np.sqrt(W)) * np.exp(ly) * jac
+    f = joint.sum()
+    return f, (joint * W).sum() / f, (joint * np.log(W)).sum() / f
+
+
+@pytest.mark.parametrize("p", [1, 2])
+def test_e1_exact_q1_vs_generative_quadrature(orc, p):
+    """Exact e1 = E[log W | y] (reading R2') vs 2-D quadrature of the generative joint at q = 1.
+    The lattice estimate is a 1-D rule over the chi node (log V is singular as V -> 0), so the
+    pin is: error <= 1e-4 at M = 2^16 and shrinking with M; the A5 approximation is >= 30x worse."""
+    rng = np.random.default_rng(13 + p)
+    mu = rng.standard_normal(p)
+    A = rng.standard_normal((p, p))
+    Sig = A @ A.T + 0.5 * np.eye(p)
+    D = rng.uniform(-2, 2, (p, 1))
+    nu = 5.5
+    for y in [mu + D[:, 0] * 0.9 + 0.2, mu - 1.0, mu + 2.5 * D[:, 0]]:
+        f, e2, e1 = _joint_grid_q1(p, mu, Sig, D, nu, y)
+        errs = []
+        for M in [1024, 65536]:
+            r = orc.pair(y, mu, Sig, D, nu, _lat(orc, M), e1_exact=True)
+            assert abs(math.exp(r["logf"]) / f - 1) < 1e-9          # density unchanged (exact T_1)
+            assert abs(r["e2"] / e2 - 1) < 1e-9
+            errs.append(abs(r["e1me2"] + r["e2"] - e1))
+        assert errs[1] < 1e-4 and errs[1] < errs[0], errs
+        r1 = orc.pair(y, mu, Sig, D, nu, None)                          # reading A5
+        assert abs(r1["e1me2"] + r1["e2"] - e1) > 30 * errs[1]
+
+
+def test_e1_exact_delta_zero_closed_form(orc):
+    """Delta = 0 (q = 3): Phi_q(0; I) = 2^-q is constant on every lattice point, so the exact e1
+    is the lattice mean of log V minus log rho -> psi(m0/2) - log(rho/2) (the A5 formula, exact
+    here); the lattice error converges with M."""
+    import scipy.special as sp
+    p, q, nu = 3, 3, 7.5
+    rng = np.random.default_rng(2)
+    A = rng.standard_normal((p, p))
+    Sig = A @ A.T + np.eye(p)
+    mu = rng.standard_normal(p)
+    y = rng.standard_normal(p)
+    d = (y - mu) @ np.linalg.solve(Sig, y - mu)
+    ref = sp.digamma((nu + p) / 2) - math.log((nu + d) / 2)
+    errs = []
+    for M in [1024, 65536]:
+        r = orc.pair(y, mu, Sig, np.zeros((p, q)), nu, _lat(orc, M), e1_exact=True)
+        errs.append(abs(r["e1me2"] + r["e2"] - ref))
+    assert errs[1] < 1e-5 and errs[1] < errs[0] / 4, errs
+
+
+def test_e1_exact_q2_vs_generative_monte_carlo(orc):
+    """Exact e1 at q = 2 vs self-normalised Monte Carlo of E[log W | y] (5 s.e.)."""
+    p, q, nu = 2, 2, 6.3
+    rng = np.random.default_rng(21)
+    mu = rng.standard_normal(p)
+    A = rng.standard_normal((p, p))
+    Sig = A @ A.T + 0.5 * np.eye(p)
+    D = rng.uniform(-2, 2, (p, q))
+    y = mu + D @ np.abs(rng.standard_normal(q)) * 0.8 + 0.3 * rng.standard_normal(p)
+    r = orc.pair(y, mu, Sig, D, nu, _lat(orc, 65536), e1_exact=True)
+    Si = np.linalg.inv(Sig)
+    vals = []
+    for _ in range(4):
+        w = rng.gamma(nu / 2, 2 / nu, 1_000_000)
+        u = np.abs(rng.standard_normal((len(w), q))) / np.sqrt(w)[:, None]
+        rr = y[None, :] - mu[None, :] - u @ D.T
+        wt = np.exp(0.5 * p * np.log(w) - 0.5 * w * np.einsum("ni,ij,nj->n", rr, Si, rr))
+        vals.append((wt * np.log(w)).sum() / wt.sum())
+    m, se = np.mean(vals), np.std(vals, ddof=1) / 2
+    assert abs(r["e1me2"] + r["e2"] - m) <= 5 * se + 1e-4, (r["e1me2"] + r["e2"], m, se)
+
+
+def test_e1_exact_estep_stats_q0_unchanged(orc):
+    """q = 0: the closed form of reading A5 is already exact; the flag changes nothing."""
+    cfg = synth.with_n(synth.CONFIGS[3], 500)
+    y, init, _ = synth.make_problem(cfg)
+    a = orc.estep(y, init, 0, None)
+    b = orc.estep(y, init, 0, None, e1_exact=True)
+    assert np.array_equal(a["stats"], b["stats"])

@@ -128,3 +128,16 @@ def test_fit_stops_with_aitken(orc):
     cfg, y, init, lat = _setup(orc, 3, 3000)
     res = orc.fit(y, init, 0, None, max_iter=500, tol=1e-6)
     assert res["converged"] and res["n_iter"] < 500
+
+
+def test_fit_e1_exact_monotone_and_differs(orc):
+    """Exact e1 (reading R2'): the nu step becomes a true CM step of the ECM, so l^(k) is
+    non-decreasing up to integration error (cfg1, 10 iterations); the nu estimates differ from
+    the reading-A5 fit (the two e1 definitions disagree at the 1e-3 level)."""
+    cfg, y, init, lat = _setup(orc, 1, 1000)
+    res = orc.fit(y, init, cfg.q, lat, max_iter=10, e1_exact=True)
+    assert res["rc"] == 0 and res["n_iter"] == 10
+    d = np.diff(res["trace"])
+    assert np.all(d > -1e-6 * np.abs(res["trace"][1:])), res["trace"]
+    ref = orc.fit(y, init, cfg.q, lat, max_iter=10)
+    assert np.max(np.abs(res["params"]["nu"] - ref["params"]["nu"]) / ref["params"]["nu"]) > 1e-4
