@@ -264,6 +264,22 @@ def main():
         t_e2e = float(tt.item())
     em_h.close()
 
+    # NEXT rows on the same workload, E-step kernel time only: exact e1 (NEXT-2)
+    next_rows = {}
+    if cfg.q >= 1:
+        em_x = cf.CfustEM(yd, cfg.g, cfg.q, init, synth.lattice_inputs(cfg, e1_exact=True), n_total=cfg.n,
+                          rank=rank, world=world, nccl_id=nccl_id_e2e(world, rank, cf, dist) if world > 1 else None,
+                          device=local, timing=True, e1_exact=True)
+        em_x.estep()
+        em_x.timing(reset=True)
+        for _ in range(2):
+            em_x.estep()
+        xms, xcnt = em_x.timing(reset=True)
+        x_est = xms[0] / max(1, xcnt[0])
+        next_rows["e1_exact"] = {"estep_ms": x_est, "pairs_per_s": (j1 - j0) * cfg.g / (x_est * 1e-3),
+                                 "overhead_vs_default": x_est / (phase_ms[0] / max(1, phase_cnt[0])) - 1.0}
+        em_x.close()
+
     est_ms = phase_ms[0] / max(1, phase_cnt[0])
     pairs_local = (j1 - j0) * cfg.g
     evals = sov_evals_per_pair(cfg.q) * cfg.M * pairs_local
@@ -295,6 +311,7 @@ def main():
             "e2e": {"value": cfg.n * cfg.g / (t_e2e * 1e-3), "unit": UNIT,
                     "h2d_bytes_per_step": int(yl.nbytes), "d2h_bytes_per_step": 8 + 16},
             "gpu_launches": int(launches),
+            "next_rows": next_rows,
             "clocks": clk.summary()}
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(cfg, y, init)

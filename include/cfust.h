@@ -17,7 +17,8 @@
  *  - The context owns all device memory, its CUDA stream, events and (world > 1) the NCCL
  *    communicator until cfust_destroy.  No global state; one context per thread at a time.
  *  - Limits: 1 <= p <= 8, 0 <= q <= 6, 1 <= g <= 8; lattice M a power of two in
- *    [1024, 65536] when q >= 2 (q <= 1 needs no lattice).
+ *    [1024, 65536] when q >= 2 or (q == 1 and opts.e1_exact); otherwise no lattice is used.
+ *    lattice_z / lattice_shift hold max(q, 1) entries.
  *  - There is no CPU fallback: without a CUDA device every call fails with CFUST_ECUDA.
  */
 #ifndef CFUST_H
@@ -63,6 +64,11 @@ typedef struct {
     const void *nccl_id;           /* 128-byte ncclUniqueId, identical on all ranks (world > 1)    */
     int64_t n_total;               /* sum of n over ranks (pi = S0 / n_total); 0 -> n              */
     int32_t timing;                /* 1: record CUDA events per phase (see cfust_get_timing)       */
+    int32_t e1_exact;              /* 0: e1 = E[log W|y] by the closed-form approximation (reading
+                                      A5); 1: exact, estimated on T0's own lattice
+                                      points as (sum_l f_l log V_l)/(sum_l f_l) - log rho (reading
+                                      R2', NEXT-2).  With q = 1 this needs a lattice (lattice_m,
+                                      lattice_z[1], lattice_shift[1]); with q = 0 it is a no-op.  */
 } cfust_opts;
 
 typedef struct {

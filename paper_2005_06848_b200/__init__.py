@@ -57,7 +57,7 @@ class CfustEM:
 
     def __init__(self, y, g: int, q: int, init: dict, lattice=None, *, n_total: int | None = None,
                  rank: int = 0, world: int = 1, nccl_id: bytes | None = None, device: int = -1,
-                 timing: bool = False, nu_lo: float = 0.1, nu_hi: float = 1000.0):
+                 timing: bool = False, nu_lo: float = 0.1, nu_hi: float = 1000.0, e1_exact: bool = False):
         L = lib()
         self._keep = []
         on_dev = hasattr(y, "data_ptr") and getattr(y, "is_cuda", False)
@@ -75,7 +75,7 @@ class CfustEM:
         self.K = k_stats(p, q)
         prm = self._params_struct(init)
         opts = Opts()
-        if lattice is not None and q >= 2:
+        if lattice is not None and (q >= 2 or (e1_exact and q >= 1)):
             M, z, sh = lattice
             zz = np.ascontiguousarray(np.asarray(z, dtype=np.uint32))
             ss = _f64(sh)
@@ -93,6 +93,7 @@ class CfustEM:
             opts.nccl_id = C.cast(idbuf, C.c_void_p)
         opts.n_total = int(n_total) if n_total else 0
         opts.timing = 1 if timing else 0
+        opts.e1_exact = 1 if e1_exact else 0
         ctx = C.c_void_p()
         rc = L.cfust_em_init(C.byref(ctx), yptr, self.n, self.p, self.g, self.q, C.byref(prm), C.byref(opts))
         if rc != 0:

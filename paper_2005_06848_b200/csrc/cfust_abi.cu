@@ -162,7 +162,7 @@ int enqueue_estep(cfust_ctx *ctx, int mode) {
 int enqueue_mstep(cfust_ctx *ctx) {
     CUI(launch_mstep(ctx->s, ctx->stream));
     CUI(launch_chi(ctx->s, ctx->stream));
-    ctx->launches += (ctx->s.q >= 2) ? 2 : 1;
+    ctx->launches += (ctx->s.M > 0) ? 2 : 1;
     rec(ctx, 4);
     return CFUST_OK;
 }
@@ -226,14 +226,17 @@ int cfust_em_init(cfust_ctx **out, const double *y, int64_t n, int32_t p, int32_
             break;
         }
         if (n > 0 && !y) { rc = fail(ctx, CFUST_EINVAL, "y is NULL"); break; }
-        const int M = (q >= 2) ? opts->lattice_m : 0;
-        if (q >= 2) {
+        const bool use_e1 = opts->e1_exact != 0 && q >= 1;   // q = 0: reading A5 is exact
+        const bool need_lat = q >= 2 || use_e1;
+        const int M = need_lat ? opts->lattice_m : 0;
+        const int nz = q > 1 ? q : 1;                          // lattice coordinates used
+        if (need_lat) {
             if (M < 1024 || M > 65536 || (M & (M - 1)) != 0) {
                 rc = fail(ctx, CFUST_EINVAL, "lattice_m must be a power of two in [1024, 65536]");
                 break;
             }
             if (!opts->lattice_z || !opts->lattice_shift) { rc = fail(ctx, CFUST_EINVAL, "lattice z/shift NULL"); break; }
-            for (int k = 0; k < q; ++k) {
+            for (int k = 0; k < nz; ++k) {
                 if (opts->lattice_z[k] == 0 || opts->lattice_z[k] >= uint32_t(M)) { rc = fail(ctx, CFUST_EINVAL, "bad lattice z"); break; }
                 if (!(opts->lattice_shift[k] > 0.0 && opts->lattice_shift[k] < 1.0)) { rc = fail(ctx, CFUST_EINVAL, "lattice shift must be in (0,1)"); break; }
             }
@@ -265,7 +268,8 @@ int cfust_em_init(cfust_ctx **out, const double *y, int64_t n, int32_t p, int32_
         s.nu_hi = (opts->nu_hi > 0.0) ? opts->nu_hi : 1000.0;
         s.M = M;
         for (int k = 0; k < 8; ++k) { s.z[k] = 1; s.shift[k] = 0.5; }
-        for (int k = 0; k < q && M > 0; ++k) { s.z[k] = opts->lattice_z[k]; s.shift[k] = opts->lattice_shift[k]; }
+        for (int k = 0; k < nz && M > 0; ++k) { s.z[k] = opts->lattice_z[k]; s.shift[k] = opts->lattice_shift[k]; }
+        s.e1_exact = use_e1 ? 1 : 0;
         s.num_sms = prop.multiProcessorCount;
         const int GK1 = g * s.K + 1;
         auto alloc = [&](void **ptr, size_t bytes) { return cudaMalloc(ptr, bytes < 8 ? 8 : bytes) == cudaSuccess; };
@@ -273,8 +277,8 @@ int cfust_em_init(cfust_ctx **out, const double *y, int64_t n, int32_t p, int32_
                   alloc((void **)&s.sigma, sizeof(double) * g * p * p) &&
                   alloc((void **)&s.delta, sizeof(double) * g * p * (q > 0 ? q : 1)) &&
                   alloc((void **)&s.nu, sizeof(double) * g) && alloc((void **)&s.comp, comp_dev_size() * g) &&
-                  alloc((void **)&s.chi, sizeof(double) * g * 3 * (M > 0 ? M : 1)) &&
-                  alloc((void **)&s.W, sizeof(double) * (q > 0 ? q : 1) * (M > 0 ? M : 1)) &&
+                  alloc((void **)&s.chi, sizeof(double) * g * CHI_ROWS * (M > 0 ? M : 1)) &&
+                  alloc((void **)&s.W, sizeof(double) * nz * (M > 0 ? M : 1)) &&
                   alloc((void **)&s.partials, sizeof(double) * size_t(max_partial_blocks(s)) * GK1) &&
                   alloc((void **)&s.stats, sizeof(double) * GK1) && alloc((void **)&s.status, sizeof(int) * 4) &&
                   alloc((void **)&ctx->d_ll, sizeof(double));

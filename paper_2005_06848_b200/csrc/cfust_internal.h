@@ -18,7 +18,7 @@ struct DevState {
     const double *y;                // [n][p]
     double *pi, *mu, *sigma, *delta, *nu;   // Psi on device
     CompDev *comp;                  // [g]
-    double *chi;                    // [g][3][M] chi radius nodes for df m0, m0+1, m0+2
+    double *chi;                    // [g][CHI_ROWS][M]: chi radius nodes for df m0, m0+1, m0+2; log V (df m0)
     double *W;                      // [q][M] lattice coordinates (fixed per context)
     double *partials;               // [max_blocks][g*K+1]
     double *stats;                  // [g*K+1] reduced (then all-reduced) statistics
@@ -28,7 +28,11 @@ struct DevState {
     uint32_t z[8];
     double shift[8];
     int num_sms;
+    int e1_exact;                   // 1: exact e1 = E[log W | y] (reading R2'); 0: reading A5
 };
+
+// rows of the per-component node table DevState::chi
+constexpr int CHI_M1 = 1, CHI_M2 = 2, CHI_LV = 3, CHI_ROWS = 4;
 
 // Launchers (all asynchronous on `st`); return cudaError_t as int.
 int launch_estep(const DevState &s, int mode, const int64_t *idx, int64_t cnt, double *pair_out,

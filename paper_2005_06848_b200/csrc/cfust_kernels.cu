@@ -100,16 +100,18 @@ struct Tune {
                               : Q == 4 ? CFUST_MB_Q4 : Q == 5 ? CFUST_MB_Q5 : CFUST_MB_Q6;
 };
 
-template <int R, int NPTS>
+// WT: also accumulate *wacc += f_l lv_l (exact e1, reading R2': lv = log V node table).
+template <int R, int NPTS, bool WT = false>
 __device__ __forceinline__ double sov_lane_sum(const double (&binv)[R], const double (&Cn)[R * (R - 1) / 2],
                                                const double *__restrict__ chi, const double *__restrict__ W, int M,
-                                               int lane) {
+                                               int lane, const double *__restrict__ lv = nullptr,
+                                               double *wacc = nullptr) {
     // NPTS lattice points per iteration (l, l + 32, ...): independent chains for the FP64 pipe.
     // M is a power of two >= 1024, so 32 * NPTS divides it exactly when NPTS is a power of two.
     static_assert(NPTS == 1 || NPTS == 2 || NPTS == 4, "NPTS must divide M / 32");
-    double acc[NPTS];
+    double acc[NPTS], accw[NPTS];
 #pragma unroll
-    for (int j = 0; j < NPTS; ++j) acc[j] = 0.0;
+    for (int j = 0; j < NPTS; ++j) acc[j] = accw[j] = 0.0;
     for (int l0 = lane; l0 < M; l0 += 32 * NPTS) {
         double s[NPTS], e[NPTS], f[NPTS], z[NPTS][R - 1];
 #pragma unroll
@@ -135,12 +137,52 @@ __device__ __forceinline__ double sov_lane_sum(const double (&binv)[R], const do
             }
         }
 #pragma unroll
-        for (int j = 0; j < NPTS; ++j) acc[j] += f[j];
+        for (int j = 0; j < NPTS; ++j) {
+            acc[j] += f[j];
+            if constexpr (WT) accw[j] = fma(f[j], __ldg(lv + l0 + 32 * j), accw[j]);
+        }
     }
-    double tot = 0.0;
+    double tot = 0.0, totw = 0.0;
 #pragma unroll
-    for (int j = 0; j < NPTS; ++j) tot += acc[j];
+    for (int j = 0; j < NPTS; ++j) { tot += acc[j]; totw += accw[j]; }
+    if constexpr (WT) *wacc = totw;
     return tot;
+}
+
+// Reordering (ascending b_k / sqrt(S_kk), stable; reading A13) and the scaled Cholesky factors of
+// the SOV: binv_k = b_perm(k) / C_kk, Cn_kt = C_kt / C_kk.  false if S is not PD.
+template <int R>
+__device__ __forceinline__ bool sov_setup(const double *b, const double *S, int lds, double (&binv)[R],
+                                          double (&Cn)[R * (R - 1) / 2]) {
+    int perm[R];
+    double key[R];
+#pragma unroll
+    for (int k = 0; k < R; ++k) { perm[k] = k; key[k] = b[k] / sqrt(S[k * lds + k]); }
+    for (int i = 1; i < R; ++i) {
+        const int pi = perm[i];
+        int j = i - 1;
+        while (j >= 0 && key[perm[j]] > key[pi]) { perm[j + 1] = perm[j]; --j; }
+        perm[j + 1] = pi;
+    }
+    double C[R][R];
+    for (int i = 0; i < R; ++i)
+        for (int j = 0; j <= i; ++j) {
+            double s = S[perm[i] * lds + perm[j]];
+            for (int k = 0; k < j; ++k) s -= C[i][k] * C[j][k];
+            if (i == j) {
+                if (!(s > 1e-300)) return false;
+                C[i][i] = sqrt(s);
+            } else {
+                C[i][j] = s / C[j][j];
+            }
+        }
+#pragma unroll
+    for (int k = 0; k < R; ++k) binv[k] = b[perm[k]] / C[k][k];
+#pragma unroll
+    for (int k = 1; k < R; ++k)
+#pragma unroll
+        for (int t = 0; t < k; ++t) Cn[(k * (k - 1)) / 2 + t] = C[k][t] / C[k][k];
+    return true;
 }
 
 // T_R(b; 0, S, m): R = 0 -> 1; R = 1 -> univariate t CDF; R >= 2 -> lattice rule with
@@ -154,45 +196,42 @@ __device__ __noinline__ double T_eval(const double *b, const double *S, int lds,
     } else if constexpr (R == 1) {
         return dev_t_cdf(b[0] / sqrt(S[0]), m);
     } else {
-        int perm[R];
-        double key[R];
-#pragma unroll
-        for (int k = 0; k < R; ++k) { perm[k] = k; key[k] = b[k] / sqrt(S[k * lds + k]); }
-        for (int i = 1; i < R; ++i) {
-            const int pi = perm[i];
-            int j = i - 1;
-            while (j >= 0 && key[perm[j]] > key[pi]) { perm[j + 1] = perm[j]; --j; }
-            perm[j + 1] = pi;
-        }
-        double C[R][R];
-        for (int i = 0; i < R; ++i)
-            for (int j = 0; j <= i; ++j) {
-                double s = S[perm[i] * lds + perm[j]];
-                for (int k = 0; k < j; ++k) s -= C[i][k] * C[j][k];
-                if (i == j) {
-                    if (!(s > 1e-300)) return CUDART_NAN;
-                    C[i][i] = sqrt(s);
-                } else {
-                    C[i][j] = s / C[j][j];
-                }
-            }
         double binv[R], Cn[R * (R - 1) / 2];
-#pragma unroll
-        for (int k = 0; k < R; ++k) binv[k] = b[perm[k]] / C[k][k];
-#pragma unroll
-        for (int k = 1; k < R; ++k)
-#pragma unroll
-            for (int t = 0; t < k; ++t) Cn[(k * (k - 1)) / 2 + t] = C[k][t] / C[k][k];
+        if (!sov_setup<R>(b, S, lds, binv, Cn)) return CUDART_NAN;
         const double acc = sov_lane_sum<R, NP>(binv, Cn, chi, W, M, lane);
         return warp_sum(acc) / double(M);
     }
+}
+
+// T_R on the lattice together with *wsum = (1/M) sum_l f_l lv_l over the same points (exact e1,
+// reading R2'); R = 1 is evaluated on the lattice here too (f_l = Phi(s_l b / sqrt(S))).
+template <int R, int NP>
+__device__ __noinline__ double T_eval_w(const double *b, const double *S, int lds, const double *__restrict__ chi,
+                                        const double *__restrict__ lv, const double *__restrict__ W, int M, int lane,
+                                        double *wsum) {
+    static_assert(R >= 1, "T_eval_w: R >= 1");
+    double acc = 0.0, accw = 0.0;
+    if constexpr (R == 1) {
+        const double bs = b[0] / sqrt(S[0]);
+        for (int l = lane; l < M; l += 32) {
+            const double f = Phi(__ldg(chi + l) * bs);
+            acc += f;
+            accw = fma(f, __ldg(lv + l), accw);
+        }
+    } else {
+        double binv[R], Cn[R * (R - 1) / 2];
+        if (!sov_setup<R>(b, S, lds, binv, Cn)) { *wsum = CUDART_NAN; return CUDART_NAN; }
+        acc = sov_lane_sum<R, NP, true>(binv, Cn, chi, W, M, lane, lv, &accw);
+    }
+    *wsum = warp_sum(accw) / double(M);
+    return warp_sum(acc) / double(M);
 }
 
 // Per pair (observation in ws.y, component cp): O2-O8 of DESIGN.md §3.
 // MODE 1 computes only log f (T0).  Results go to res[] (identical in all lanes).
 template <int Q, int MODE>
 __device__ void pair_eval(const CompDev &cp, int p, const double *__restrict__ W, int M, const double *__restrict__ chi,
-                          WarpScratch &ws, double *res, int lane) {
+                          WarpScratch &ws, double *res, int lane, int e1_exact) {
     double r[PMAX], v[PMAX];
     double d = 0.0;
 #pragma unroll
@@ -221,7 +260,15 @@ __device__ void pair_eval(const CompDev &cp, int p, const double *__restrict__ W
     const double sq0 = sqrt(m0 / rho);
 #pragma unroll
     for (int k = 0; k < Q; ++k) ws.b[k] = c[k] * sq0;
-    const double T0 = T_eval<Q, Tune<Q>::NP>(ws.b, cp.Lam, QMAX, m0, chi, W, M, lane);
+    double T0, e1x = 0.0;
+    if (MODE != 1 && e1_exact) {   // exact e1 = (sum f lv)/(sum f) - log rho on T0's points (R2')
+        double wsum;
+        const double T0lat = T_eval_w<Q, Tune<Q>::NP>(ws.b, cp.Lam, QMAX, chi, chi + CHI_LV * M, W, M, lane, &wsum);
+        T0 = (Q == 1) ? T_eval<1, 1>(ws.b, cp.Lam, QMAX, m0, chi, W, M, lane) : T0lat;   // density: exact T_1
+        e1x = wsum / T0lat - log(rho);
+    } else {
+        T0 = T_eval<Q, Tune<Q>::NP>(ws.b, cp.Lam, QMAX, m0, chi, W, M, lane);
+    }
     if (MODE == 1) {
         res[0] = (T0 > 0.0) ? Q * CUDART_LN2 + logt + log(T0) : -CUDART_INF;
         return;
@@ -229,7 +276,7 @@ __device__ void pair_eval(const CompDev &cp, int p, const double *__restrict__ W
     const double sq2 = sqrt((m0 + 2.0) / rho);
 #pragma unroll
     for (int k = 0; k < Q; ++k) ws.b[k] = c[k] * sq2;
-    const double T2 = T_eval<Q, Tune<Q>::NP>(ws.b, cp.Lam, QMAX, m0 + 2.0, chi + 2 * M, W, M, lane);
+    const double T2 = T_eval<Q, Tune<Q>::NP>(ws.b, cp.Lam, QMAX, m0 + 2.0, chi + CHI_M2 * M, W, M, lane);
     res[1] = cp.psi_half_m0 - log(0.5 * rho) - m0 / rho;      // e1 - e2, reading A5
     if (!(T0 > 0.0)) {                                          // reading A16
         res[0] = -CUDART_INF;
@@ -299,7 +346,7 @@ __device__ void pair_eval(const CompDev &cp, int p, const double *__restrict__ W
 #pragma unroll
     for (int k = 0; k < Q; ++k) {
         double tk = 1.0;
-        if constexpr (Q >= 2) tk = T_eval<Q1, Tune<Q>::NP>(ws.ct[k], ws.St[k], QMAX, m0 + 1.0, chi + M, W, M, lane);
+        if constexpr (Q >= 2) tk = T_eval<Q1, Tune<Q>::NP>(ws.ct[k], ws.St[k], QMAX, m0 + 1.0, chi + CHI_M1 * M, W, M, lane);
         ws.Tk[k] = tk;
         h[k] = ws.phi[k] * tk;
     }
@@ -340,6 +387,7 @@ __device__ void pair_eval(const CompDev &cp, int p, const double *__restrict__ W
     const double inv = 1.0 / T0;
     res[0] = Q * CUDART_LN2 + logt + log(T0);
     res[2] = fr * T2 * inv;
+    if (e1_exact) res[1] = e1x - res[2];
 #pragma unroll
     for (int a = 0; a < Q; ++a) res[3 + a] = fr * E1[a] * inv;
     double E2[Q][Q];
@@ -397,6 +445,7 @@ struct EArgs {
     const int64_t *__restrict__ idx;
     int64_t cnt;
     double *__restrict__ pair_out;
+    int e1_exact;                   // 1: exact e1 (reading R2'), 0: reading A5
 };
 
 // MODE 0: E-step statistics; 1: log-likelihood only; 2: per-pair dump of idx[0..cnt).
@@ -426,7 +475,8 @@ __global__ void __launch_bounds__(EW * 32, Tune<Q>::MB) estep_cfust_kernel(EArgs
         if (lane < p) ws.y[lane] = A.y[j * p + lane];
         __syncwarp();
         for (int i = 0; i < g; ++i)
-            pair_eval<Q, MODE == 1 ? 1 : 0>(comp[i], p, A.W, M, A.chi + size_t(i) * 3 * M, ws, ws.res[i], lane);
+            pair_eval<Q, MODE == 1 ? 1 : 0>(comp[i], p, A.W, M, A.chi + size_t(i) * CHI_ROWS * M, ws, ws.res[i], lane,
+                                            A.e1_exact);
         __syncwarp();
         // Eq. (3)-(4): LSE over components, tau
         double lf[GMAX], mx = -CUDART_INF;
@@ -930,21 +980,26 @@ __global__ void mstep_kernel(DevState s) {
     }
 }
 
-// chi radius nodes: chi[(i*3 + k)*M + l] = sqrt(chi2_{m0+k}^{-1}(w_{l,0}) / (m0+k))
+// chi radius nodes: chi[(i*CHI_ROWS + k)*M + l] = sqrt(chi2_{m0+k}^{-1}(w_{l,0}) / (m0+k)), k = 0,1,2;
+// row CHI_LV = log chi2_{m0}^{-1}(w_{l,0}) = log V_l (exact e1, reading R2').
 __global__ void chi_kernel(DevState s) {
     const int M = s.M;
-    const int total = s.g * 3 * M;
+    const int total = s.g * CHI_ROWS * M;
     for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < total; t += gridDim.x * blockDim.x) {
-        const int l = t % M, ik = t / M, i = ik / 3, k = ik % 3;
-        const double m = s.comp[i].m0 + double(k);
+        const int l = t % M, ik = t / M, i = ik / CHI_ROWS, k = ik % CHI_ROWS;
         const double w = s.W[l];   // coordinate 0 drives the chi radius
-        s.chi[t] = sqrt(dev_chi2_quantile(w, m) / m);
+        if (k == CHI_LV) {   // only used (and only computed) with exact e1
+            if (s.e1_exact) s.chi[t] = log(dev_chi2_quantile(w, s.comp[i].m0));
+        } else {
+            const double m = s.comp[i].m0 + double(k);
+            s.chi[t] = sqrt(dev_chi2_quantile(w, m) / m);
+        }
     }
 }
 
 // lattice coordinates W[k][l] = |2 frac((l z_k mod M)/M + shift_k) - 1|, once per context
 __global__ void lattice_kernel(DevState s, LatticeDev L) {
-    const int total = s.q * s.M;
+    const int total = (s.q > 1 ? s.q : 1) * s.M;
     for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < total; t += gridDim.x * blockDim.x)
         s.W[t] = lattice_w(L, t % s.M, t / s.M);
 }
@@ -1088,6 +1143,7 @@ int launch_estep(const DevState &s, int mode, const int64_t *idx, int64_t cnt, d
     a.idx = idx;
     a.cnt = cnt;
     a.pair_out = pair_out;
+    a.e1_exact = s.e1_exact;
     *nblocks_out = 0;
     if (s.q == 0) {
         if (mode == 2) {
@@ -1136,16 +1192,16 @@ int launch_derive(const DevState &s, cudaStream_t st) {
 }
 
 int launch_chi(const DevState &s, cudaStream_t st) {
-    if (s.q < 2 || s.M <= 0) return 0;
-    const int total = s.g * 3 * s.M;
+    if (s.M <= 0) return 0;   // no lattice: q <= 1 without exact e1
+    const int total = s.g * CHI_ROWS * s.M;
     chi_kernel<<<(total + 127) / 128, 128, 0, st>>>(s);
     return int(cudaGetLastError());
 }
 
 int launch_lattice(const DevState &s, cudaStream_t st) {
-    if (s.q < 2 || s.M <= 0) return 0;
+    if (s.M <= 0) return 0;
     const LatticeDev L = make_lattice(s);
-    const int total = s.q * s.M;
+    const int total = (s.q > 1 ? s.q : 1) * s.M;
     lattice_kernel<<<(total + 127) / 128, 128, 0, st>>>(s, L);
     return int(cudaGetLastError());
 }

@@ -173,8 +173,12 @@ def lattice_dims(q: int) -> int:
     return q if q >= 2 else 0
 
 
-def lattice_inputs(cfg: Config) -> tuple[int, np.ndarray, np.ndarray]:
+def lattice_inputs(cfg: Config, e1_exact: bool = False) -> tuple[int, np.ndarray, np.ndarray]:
+    """(M, z, shift).  e1_exact with q = 1 needs the one chi coordinate (reading R2')."""
     s = lattice_dims(cfg.q)
+    if e1_exact and cfg.q == 1:
+        M = cfg.M or 1024
+        return M, lattice_z(M, 1), lattice_shift(cfg.lattice_seed, 1)
     if s == 0:
         return 0, np.zeros(1, np.uint32), np.zeros(1)
     return cfg.M, lattice_z(cfg.M, s), lattice_shift(cfg.lattice_seed, s)

@@ -267,3 +267,41 @@ def test_shard_additivity(cf):
         em.close()
     assert np.max(np.abs(acc - st) / np.maximum(np.abs(st), 1e-300)) < 1e-11
     full.close()
+
+
+# ------------------------------------------------------------------ exact e1 (NEXT-2, reading R2')
+def _problem_e1(cfg_id, n, **kw):
+    cfg = synth.with_n(synth.CONFIGS[cfg_id], n)
+    if kw:
+        cfg = synth.with_(cfg, **kw)
+    y, init, _ = synth.make_problem(cfg)
+    return cfg, y, init, synth.lattice_inputs(cfg, e1_exact=True)
+
+
+@pytest.mark.parametrize("cfg_id,n,kw", [(1, 700, {}), (2, 211, {}), (4, 29, {}), (5, 257, {}),
+                                         (1, 301, {"q": 1, "g": 2})])
+def test_e1_exact_pairs_and_stats_parity(cf, orc, cfg_id, n, kw):
+    cfg, y, init, lat = _problem_e1(cfg_id, n, **kw)
+    em = cf.CfustEM(y, cfg.g, cfg.q, init, lat, e1_exact=True)
+    got = em.pairs(np.arange(n))
+    ref = orc.estep(y, init, cfg.q, _olat(orc, lat), pairs=True, gaps=True, e1_exact=True)
+    compare_pairs(got, ref["pairs"], cfg.q, ref["gaps"])
+    # the e1 column really is the exact one (differs from reading A5 beyond the tolerance)
+    a5 = orc.estep(y, init, cfg.q, _olat(orc, lat), pairs=True)["pairs"]
+    assert np.max(np.abs(a5[..., 2] - ref["pairs"][..., 2])) > 1e-6
+    ll, st = em.estep(want_stats=True)
+    compare_stats(st, ref["stats"], cfg.p, cfg.q, cfg.g)
+    em.close()
+
+
+@pytest.mark.parametrize("cfg_id,n,iters", [(1, 1000, 10), (5, 200, 5)])
+def test_e1_exact_fit_parity(cf, orc, cfg_id, n, iters):
+    cfg, y, init, lat = _problem_e1(cfg_id, n)
+    em = cf.CfustEM(y, cfg.g, cfg.q, init, lat, e1_exact=True)
+    res = em.fit(iters)
+    ref = orc.fit(y, init, cfg.q, _olat(orc, lat), max_iter=iters, e1_exact=True)
+    assert ref["rc"] == 0 and res["n_iter"] == ref["n_iter"] == iters
+    tr_err = np.max(np.abs(res["trace"] - ref["trace"]) / np.abs(ref["trace"]))
+    assert tr_err <= TOL, tr_err
+    compare_params(res["params"], ref["params"], cfg.q)
+    em.close()
