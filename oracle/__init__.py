@@ -85,6 +85,21 @@ def lib():
                               _I, _I, _I, _D, _D, _D, _PD, C.POINTER(_I), C.POINTER(_I)]
         L.orc_k_stats.restype = _I
         L.orc_k_stats.argtypes = [_I, _I]
+        _U64 = C.c_uint64
+        _PI32 = C.POINTER(C.c_int32)
+        L.orc_splitmix64.restype = _U64
+        L.orc_splitmix64.argtypes = [_U64]
+        L.orc_random_label.restype = _I
+        L.orc_random_label.argtypes = [_U64, _I64, _I64, _I]
+        L.orc_random_partition.restype = _I
+        L.orc_random_partition.argtypes = [_I64, _I, _I, _U64, _I, _I, _PI32]
+        L.orc_kmeans.restype = _I
+        L.orc_kmeans.argtypes = [_I64, _I, _I, _PD, _U64, _I, _PI32, _PD]
+        L.orc_partition_params.restype = _I
+        L.orc_partition_params.argtypes = [_I64, _I, _I, _I, _PD, _PI32, _D, _PD, _PD, _PD, _PD, _PD]
+        L.orc_init_select.restype = _I
+        L.orc_init_select.argtypes = [_I64, _I, _I, _I, _PD, _I, _PI32, C.POINTER(_Lattice), _I, _I, _PD,
+                                      C.POINTER(_I), _PD, _PD, _PD, _PD, _PD]
     return _lib
 
 
@@ -253,3 +268,59 @@ def fit(y, params: dict, q: int, lat: Lattice | None, max_iter: int, tol: float 
                   "delta": de.reshape(g, p, q) if q > 0 else np.zeros((g, p, 0)), "nu": nu}
     return {"rc": rc, "params": params_out, "trace": trace[:ni.value + 1], "n_iter": ni.value,
             "converged": bool(cv.value)}
+
+
+# --------------------------------------------------------------------- Alg. 1 (NEXT-1), readings I1-I4
+def _i32p(a: np.ndarray):
+    return a.ctypes.data_as(C.POINTER(C.c_int32))
+
+
+def splitmix64(x: int) -> int:
+    return int(lib().orc_splitmix64(C.c_uint64(x & 0xFFFFFFFFFFFFFFFF)))
+
+
+def random_partition(n: int, p: int, g: int, seed: int, l: int, m: int):
+    """(attempt, labels[n]) of candidate l (reading I1)."""
+    lab = np.zeros(n, dtype=np.int32)
+    a = lib().orc_random_partition(int(n), int(p), int(g), C.c_uint64(seed), int(l), int(m), _i32p(lab))
+    return a, lab
+
+
+def kmeans(y, g: int, seed: int, iters: int):
+    """(rc, labels[n], centres[g, p]) by reading I2."""
+    y = _f64(y)
+    n, p = y.shape
+    lab = np.zeros(n, dtype=np.int32)
+    cen = np.zeros((g, p))
+    rc = lib().orc_kmeans(n, p, int(g), _p(y), C.c_uint64(seed), int(iters), _i32p(lab), _p(cen))
+    return rc, lab, cen
+
+
+def partition_params(y, labels, g: int, q: int, n_total=None):
+    """(rc, Psi^(0)) from a hard partition (reading I3)."""
+    y = _f64(y)
+    n, p = y.shape
+    lab = np.ascontiguousarray(np.asarray(labels, dtype=np.int32))
+    out = {"pi": np.zeros(g), "mu": np.zeros((g, p)), "sigma": np.zeros((g, p, p)),
+           "delta": np.zeros((g, p, max(q, 1))), "nu": np.zeros(g)}
+    rc = lib().orc_partition_params(n, p, int(q), int(g), _p(y), _i32p(lab), float(n_total or n), _p(out["pi"]),
+                                    _p(out["mu"]), _p(out["sigma"]), _p(out["delta"]), _p(out["nu"]))
+    out["delta"] = out["delta"][:, :, :q].copy() if q > 0 else np.zeros((g, p, 0))
+    return rc, out
+
+
+def init_select(y, labels, g: int, q: int, lat: Lattice | None, burn_in: int = 0, nthreads=None):
+    """Alg. 1 lines 3-12 (readings I3, I4): dict(rc, loglik0[m], best, params)."""
+    y = _f64(y)
+    n, p = y.shape
+    lab = np.ascontiguousarray(np.asarray(labels, dtype=np.int32))
+    m = lab.shape[0]
+    ll = np.zeros(m)
+    best = C.c_int(-1)
+    out = {"pi": np.zeros(g), "mu": np.zeros((g, p)), "sigma": np.zeros((g, p, p)),
+           "delta": np.zeros((g, p, max(q, 1))), "nu": np.zeros(g)}
+    rc = lib().orc_init_select(n, p, int(q), int(g), _p(y), int(m), _i32p(lab), lat.ptr if lat is not None else None,
+                               _nt(nthreads), int(burn_in), _p(ll), C.byref(best), _p(out["pi"]), _p(out["mu"]),
+                               _p(out["sigma"]), _p(out["delta"]), _p(out["nu"]))
+    out["delta"] = out["delta"][:, :, :q].copy() if q > 0 else np.zeros((g, p, 0))
+    return {"rc": rc, "loglik0": ll, "best": best.value, "params": out}

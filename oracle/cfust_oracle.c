@@ -784,3 +784,190 @@ int orc_fit(int64_t n, int p, int q, int g, const double *y, double *pi, double 
     free(stats);
     return rc;
 }
+
+/* =====================================================================================
+ * Alg. 1: parallel multi-start initialisation (NEXT-1).
+ * The paper leaves open how the m partitions and Psi^(0) are made ("k-means or random
+ * partitions", "computes Psi^(0) based on the given initial partition"); the readings I1-I4
+ * of DESIGN.md §3 fix them:
+ *   I1 random partitions: label_j = (splitmix64(splitmix64(splitmix64(seed) ^ stream) ^ j) >> 32)
+ *      mod g, stream = l + m * attempt; redrawn (attempt + 1) while a component has < p+1 members.
+ *   I2 k-means: first centre y_{j*}, j* = splitmix64(seed ^ 0xA5A5A5A5A5A5A5A5) mod n; centre k
+ *      = argmax_j min_{c<k} |y_j - centre_c|^2 (farthest point, ties -> lowest j); Lloyd
+ *      iterations (nearest centre, ties -> lowest index; centre = member mean; an empty cluster
+ *      is re-seeded to the point farthest from its centre) until no label changes or `iters`.
+ *      Squared distances are accumulated as d = fma(t, t, d) over ascending coordinates.
+ *   I3 Psi^(0) from a partition: pi_i = n_i / n, ybar_i, S_i = (1/n_i) sum (y - ybar)(y - ybar)',
+ *      gamma_ik = (1/n_i) sum (y_k - ybar_k)^3; Delta_i[k][k] = 0.5 sgn(gamma_ik) sqrt(S_ikk) for
+ *      k < min(p, q) (0 elsewhere), mu_i = ybar_i - sqrt(2/pi) Delta_i 1_q, Sigma_i = S_i,
+ *      nu_i = 10.  Invalid (candidate skipped) if n_i < p+1 or S_i is not PD.
+ *   I4 selection: the LARGEST l^(0) (reading A9), ties -> lowest candidate index; with r > 0
+ *      burn-in EM iterations the candidate's l is the log-likelihood after them.
+ * ===================================================================================== */
+uint64_t orc_splitmix64(uint64_t x) {
+    uint64_t z = x + 0x9E3779B97F4A7C15ULL;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+    return z ^ (z >> 31);
+}
+
+int orc_random_label(uint64_t seed, int64_t stream, int64_t j, int g) {
+    const uint64_t h = orc_splitmix64(orc_splitmix64(orc_splitmix64(seed) ^ (uint64_t)stream) ^ (uint64_t)j);
+    return (int)((h >> 32) % (uint64_t)g);
+}
+
+int orc_random_partition(int64_t n, int p, int g, uint64_t seed, int l, int m, int32_t *labels) {
+    int64_t cnt[16];
+    for (int attempt = 0; attempt < 1000; ++attempt) {
+        for (int i = 0; i < g; ++i) cnt[i] = 0;
+        for (int64_t j = 0; j < n; ++j) {
+            labels[j] = orc_random_label(seed, (int64_t)l + (int64_t)m * attempt, j, g);
+            cnt[labels[j]]++;
+        }
+        int ok = 1;
+        for (int i = 0; i < g; ++i) if (cnt[i] < p + 1) ok = 0;
+        if (ok) return attempt;
+    }
+    return ORC_EINVAL;   /* PartitionInfeasible */
+}
+
+static double sqdist(int p, const double *a, const double *b) {
+    double d = 0.0;
+    for (int k = 0; k < p; ++k) {
+        const double t = a[k] - b[k];
+        d = fma(t, t, d);
+    }
+    return d;
+}
+
+int orc_kmeans(int64_t n, int p, int g, const double *y, uint64_t seed, int iters, int32_t *labels,
+               double *centers) {
+    if (n < g) return ORC_EINVAL;
+    double *mind = (double *)malloc(sizeof(double) * n);
+    const int64_t j0 = (int64_t)(orc_splitmix64(seed ^ 0xA5A5A5A5A5A5A5A5ULL) % (uint64_t)n);
+    memcpy(centers, y + j0 * p, sizeof(double) * p);
+    for (int64_t j = 0; j < n; ++j) mind[j] = sqdist(p, y + j * p, centers);
+    for (int k = 1; k < g; ++k) {                       /* farthest point */
+        int64_t best = 0;
+        for (int64_t j = 1; j < n; ++j) if (mind[j] > mind[best]) best = j;
+        memcpy(centers + k * p, y + best * p, sizeof(double) * p);
+        for (int64_t j = 0; j < n; ++j) {
+            const double d = sqdist(p, y + j * p, centers + k * p);
+            if (d < mind[j]) mind[j] = d;
+        }
+    }
+    for (int64_t j = 0; j < n; ++j) labels[j] = -1;
+    for (int it = 0; it < iters; ++it) {
+        int64_t changed = 0;
+        for (int64_t j = 0; j < n; ++j) {                /* assignment */
+            int bi = 0;
+            double bd = sqdist(p, y + j * p, centers);
+            for (int i = 1; i < g; ++i) {
+                const double d = sqdist(p, y + j * p, centers + i * p);
+                if (d < bd) { bd = d; bi = i; }
+            }
+            if (labels[j] != bi) { labels[j] = bi; ++changed; }
+            mind[j] = bd;
+        }
+        if (changed == 0) break;
+        double sum[16 * PMAX];
+        int64_t cnt[16];
+        memset(sum, 0, sizeof(sum));
+        memset(cnt, 0, sizeof(cnt));
+        for (int64_t j = 0; j < n; ++j) {                /* update */
+            cnt[labels[j]]++;
+            for (int k = 0; k < p; ++k) sum[labels[j] * p + k] += y[j * p + k];
+        }
+        for (int i = 0; i < g; ++i) {
+            if (cnt[i] > 0) {
+                for (int k = 0; k < p; ++k) centers[i * p + k] = sum[i * p + k] / (double)cnt[i];
+            } else {                                      /* empty: re-seed to the farthest point */
+                int64_t best = 0;
+                for (int64_t j = 1; j < n; ++j) if (mind[j] > mind[best]) best = j;
+                memcpy(centers + i * p, y + best * p, sizeof(double) * p);
+                mind[best] = 0.0;
+            }
+        }
+    }
+    free(mind);
+    return ORC_OK;
+}
+
+int orc_partition_params(int64_t n, int p, int q, int g, const double *y, const int32_t *labels,
+                         double n_total, double *pi, double *mu, double *sigma, double *delta, double *nu) {
+    for (int i = 0; i < g; ++i) {
+        int64_t ni = 0;
+        double ybar[PMAX] = {0};
+        for (int64_t j = 0; j < n; ++j)
+            if (labels[j] == i) {
+                ++ni;
+                for (int k = 0; k < p; ++k) ybar[k] += y[j * p + k];
+            }
+        if (ni < p + 1) return ORC_EINVAL;
+        for (int k = 0; k < p; ++k) ybar[k] /= (double)ni;
+        double S[PMAX * PMAX] = {0}, gam[PMAX] = {0};
+        for (int64_t j = 0; j < n; ++j)
+            if (labels[j] == i) {
+                double t[PMAX];
+                for (int k = 0; k < p; ++k) t[k] = y[j * p + k] - ybar[k];
+                for (int a = 0; a < p; ++a) {
+                    for (int b = 0; b < p; ++b) S[a * p + b] += t[a] * t[b];
+                    gam[a] += t[a] * t[a] * t[a];
+                }
+            }
+        for (int a = 0; a < p * p; ++a) S[a] /= (double)ni;
+        double Lt[PMAX * PMAX];
+        if (chol(p, S, Lt) != ORC_OK) return ORC_ENOTPD;
+        double *Di = delta + (size_t)i * p * q;
+        for (int a = 0; a < p * q; ++a) Di[a] = 0.0;
+        for (int k = 0; k < p && k < q; ++k) Di[k * q + k] = (gam[k] < 0.0 ? -0.5 : 0.5) * sqrt(S[k * p + k]);
+        for (int a = 0; a < p; ++a) {
+            double s = 0.0;
+            for (int k = 0; k < q; ++k) s += Di[a * q + k];
+            mu[i * p + a] = ybar[a] - sqrt(2.0 / ORC_PI) * s;
+        }
+        memcpy(sigma + (size_t)i * p * p, S, sizeof(double) * p * p);
+        nu[i] = 10.0;
+        pi[i] = (double)ni / n_total;
+    }
+    return ORC_OK;
+}
+
+/* Alg. 1 lines 3-12 for given partitions: Psi^(0) (I3), optional r burn-in EM iterations,
+ * l per candidate (-inf when invalid), selection I4.  params_out receive the winner's Psi. */
+int orc_init_select(int64_t n, int p, int q, int g, const double *y, int m, const int32_t *labels,
+                    const orc_lattice *L, int nthreads, int burn_in, double *loglik0, int *best,
+                    double *pi, double *mu, double *sigma, double *delta, double *nu) {
+    double *cp = (double *)malloc(sizeof(double) * (size_t)(g * (1 + p + p * p + p * (q > 0 ? q : 1) + 1)));
+    double *bpi = cp, *bmu = bpi + g, *bsg = bmu + (size_t)g * p, *bde = bsg + (size_t)g * p * p;
+    double *bnu = bde + (size_t)g * p * (q > 0 ? q : 1);
+    *best = -1;
+    for (int c = 0; c < m; ++c) {
+        loglik0[c] = -INFINITY;
+        int rc = orc_partition_params(n, p, q, g, y, labels + (size_t)c * n, (double)n, bpi, bmu, bsg, bde, bnu);
+        if (rc != ORC_OK) continue;
+        double ll;
+        if (burn_in > 0) {
+            double *trace = (double *)malloc(sizeof(double) * (burn_in + 1));
+            int ni = 0, cv = 0;
+            rc = orc_fit(n, p, q, g, y, bpi, bmu, bsg, bde, bnu, L, nthreads, 0, burn_in, 0.0, 0.1, 1000.0,
+                         trace, &ni, &cv);
+            ll = trace[ni];
+            free(trace);
+        } else {
+            rc = orc_estep(n, p, q, g, y, bpi, bmu, bsg, bde, bnu, L, nthreads, 0, NULL, NULL, &ll, NULL);
+        }
+        if (rc != ORC_OK || !(ll > -INFINITY)) continue;
+        loglik0[c] = ll;
+        if (*best < 0 || ll > loglik0[*best]) {
+            *best = c;
+            memcpy(pi, bpi, sizeof(double) * g);
+            memcpy(mu, bmu, sizeof(double) * g * p);
+            memcpy(sigma, bsg, sizeof(double) * g * p * p);
+            if (q > 0) memcpy(delta, bde, sizeof(double) * g * p * q);
+            memcpy(nu, bnu, sizeof(double) * g);
+        }
+    }
+    free(cp);
+    return *best >= 0 ? ORC_OK : ORC_EINVAL;
+}

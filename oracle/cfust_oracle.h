@@ -90,6 +90,19 @@ int orc_fit(int64_t n, int p, int q, int g, const double *y, double *pi, double 
 
 int orc_k_stats(int p, int q);
 
+/* ---- Alg. 1, readings I1-I4 ---- */
+uint64_t orc_splitmix64(uint64_t x);
+int orc_random_label(uint64_t seed, int64_t stream, int64_t j, int g);
+/* returns the attempt used (>= 0) or ORC_EINVAL when every attempt leaves a component < p+1 */
+int orc_random_partition(int64_t n, int p, int g, uint64_t seed, int l, int m, int32_t *labels);
+int orc_kmeans(int64_t n, int p, int g, const double *y, uint64_t seed, int iters, int32_t *labels,
+               double *centers);
+int orc_partition_params(int64_t n, int p, int q, int g, const double *y, const int32_t *labels,
+                         double n_total, double *pi, double *mu, double *sigma, double *delta, double *nu);
+int orc_init_select(int64_t n, int p, int q, int g, const double *y, int m, const int32_t *labels,
+                    const orc_lattice *L, int nthreads, int burn_in, double *loglik0, int *best,
+                    double *pi, double *mu, double *sigma, double *delta, double *nu);
+
 #ifdef __cplusplus
 }
 #endif

@@ -107,7 +107,7 @@ def perturb(cfg: Config, truth: dict) -> dict:
 
 
 # ----------------------------------------------------------------------------- data
-def sample(cfg: Config, truth: dict, n: int | None = None) -> np.ndarray:
+def sample(cfg: Config, truth: dict, n: int | None = None, return_labels: bool = False):
     """y_j = mu_i + Delta_i |U0| + U1, U0 ~ t_q, U1 ~ t_p(0, Sigma_i) sharing W ~ Gamma(nu/2, rate nu/2).
 
     Row-major (n, p) float64; labels drawn from pi (BASELINE.json configs, reading A18).
@@ -132,7 +132,8 @@ def sample(cfg: Config, truth: dict, n: int | None = None) -> np.ndarray:
             u0 = np.abs(rng.standard_normal((m, q))) * sw[:, None]
             yi = yi + u0 @ truth["delta"][i].T
         y[idx] = yi
-    return np.ascontiguousarray(y)
+    y = np.ascontiguousarray(y)
+    return (y, lab) if return_labels else y
 
 
 def make_problem(cfg: Config, n: int | None = None) -> tuple[np.ndarray, dict, dict]:
