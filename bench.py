@@ -279,6 +279,20 @@ def main():
         next_rows["e1_exact"] = {"estep_ms": x_est, "pairs_per_s": (j1 - j0) * cfg.g / (x_est * 1e-3),
                                  "overhead_vs_default": x_est / (phase_ms[0] / max(1, phase_cnt[0])) - 1.0}
         em_x.close()
+    # parallel multi-start initialisation (Alg. 1, NEXT-1): m = 8 candidates (k-means + 7 random),
+    # Psi^(0) from partition moments, one density pass each, argmax; wall time on the device stream
+    em_i = cf.CfustEM(yd, cfg.g, cfg.q, init, (M, z, sh), n_total=cfg.n, rank=rank, world=world,
+                      nccl_id=nccl_id_e2e(world, rank, cf, dist) if world > 1 else None, device=local,
+                      global_offset=j0)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    em_i.init_partitions(8, seed=2005, kmeans_iters=50, want_labels=False)
+    t1 = time.perf_counter()
+    ll0, best = em_i.init_select(8)
+    t2 = time.perf_counter()
+    next_rows["multistart_init"] = {"m": 8, "partitions_ms": (t1 - t0) * 1e3, "select_ms": (t2 - t1) * 1e3,
+                                    "best": best, "loglik0_best": float(ll0[best])}
+    em_i.close()
 
     est_ms = phase_ms[0] / max(1, phase_cnt[0])
     pairs_local = (j1 - j0) * cfg.g

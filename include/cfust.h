@@ -69,6 +69,8 @@ typedef struct {
                                       points as (sum_l f_l log V_l)/(sum_l f_l) - log rho (reading
                                       R2', NEXT-2).  With q = 1 this needs a lattice (lattice_m,
                                       lattice_z[1], lattice_shift[1]); with q = 0 it is a no-op.  */
+    int64_t global_offset;         /* global index of this shard's first observation (j0; 0 for one
+                                      rank): keys the random partitions and k-means seeding of Alg. 1 */
 } cfust_opts;
 
 typedef struct {
@@ -113,6 +115,29 @@ int cfust_fit(cfust_ctx *ctx, int32_t max_iter, double tol, cfust_result *out);
 
 int cfust_get_params(cfust_ctx *ctx, cfust_params *out);         /* copies into caller buffers */
 int cfust_set_params(cfust_ctx *ctx, const cfust_params *in);    /* validates, re-derives      */
+
+/* ---- Alg. 1: parallel multi-start initialisation (NEXT-1; readings I1-I4 of
+ * DESIGN.md §3) ----
+ * cfust_init_partitions: step 1, the m candidate hard partitions of this rank's shard, made on the
+ * device into a context-owned buffer [m][n] (int32 labels in [0, g)):
+ *   candidate 0      k-means (reading I2): first centre y_{j*}, j* = splitmix64(seed ^
+ *                    0xA5A5A5A5A5A5A5A5) mod n_total; farthest-point seeding; Lloyd iterations
+ *                    (at most kmeans_iters) with empty clusters re-seeded to the farthest point;
+ *   candidates 1..m-1  random labels (reading I1) splitmix64(splitmix64(splitmix64(seed) ^
+ *                    (l + m a)) ^ j) >> 32 mod g for global index j, redrawn (a = 1, 2, ...)
+ *                    while a component has fewer than p+1 members over all ranks.
+ * labels_out (may be NULL): host [m][n] copy.  Errors: CFUST_EINVAL (m < 1, n_total < g, or no
+ * feasible random partition within 1000 draws), CFUST_ECUDA, CFUST_ENCCL.  Collective over ranks.
+ *
+ * cfust_init_select: steps 2-12 for the m partitions (labels: host [m][n], or NULL for the buffer
+ * of cfust_init_partitions).  Per candidate: Psi^(0) from the partition moments (reading I3) on the
+ * device, `burn_in` EM iterations, then l = sum_j log f(y_j) (the density pass of cfust_loglik);
+ * invalid candidates (a component with < p+1 members or a non-PD covariance) get -inf.  Selects
+ * the LARGEST l (reading A9; ties -> lowest index), installs its Psi in the context and returns
+ * loglik0_out[m] (may be NULL) and *best_out.  CFUST_EINVAL if every candidate is invalid. */
+int cfust_init_partitions(cfust_ctx *ctx, int32_t m, uint64_t seed, int32_t kmeans_iters, int32_t *labels_out);
+int cfust_init_select(cfust_ctx *ctx, int32_t m, const int32_t *labels, int32_t burn_in, double *loglik0_out,
+                      int32_t *best_out);
 
 /* Per-pair E-step outputs for observations idx[0..cnt) (local indices) at the current Psi,
  * for parity checks: out[cnt][g][4 + q + q*q] = log(pi_i f_ij), tau_ij, e1-e2, e2, e3(q), e4(q*q).

@@ -57,7 +57,8 @@ class CfustEM:
 
     def __init__(self, y, g: int, q: int, init: dict, lattice=None, *, n_total: int | None = None,
                  rank: int = 0, world: int = 1, nccl_id: bytes | None = None, device: int = -1,
-                 timing: bool = False, nu_lo: float = 0.1, nu_hi: float = 1000.0, e1_exact: bool = False):
+                 timing: bool = False, nu_lo: float = 0.1, nu_hi: float = 1000.0, e1_exact: bool = False,
+                 global_offset: int = 0):
         L = lib()
         self._keep = []
         on_dev = hasattr(y, "data_ptr") and getattr(y, "is_cuda", False)
@@ -94,6 +95,7 @@ class CfustEM:
         opts.n_total = int(n_total) if n_total else 0
         opts.timing = 1 if timing else 0
         opts.e1_exact = 1 if e1_exact else 0
+        opts.global_offset = int(global_offset)
         ctx = C.c_void_p()
         rc = L.cfust_em_init(C.byref(ctx), yptr, self.n, self.p, self.g, self.q, C.byref(prm), C.byref(opts))
         if rc != 0:
@@ -173,6 +175,27 @@ class CfustEM:
         self._check(lib().cfust_get_pairs(self._ctx, idx.ctypes.data_as(C.POINTER(C.c_int64)), len(idx),
                                           _dptr(out)), "cfust_get_pairs")
         return out
+
+    def init_partitions(self, m: int, seed: int, kmeans_iters: int = 50, want_labels: bool = True):
+        """Alg. 1 step 1 (readings I1, I2): candidate 0 k-means, 1..m-1 random; labels [m, n]."""
+        out = np.zeros((m, self.n), dtype=np.int32) if want_labels else None
+        self._check(lib().cfust_init_partitions(self._ctx, int(m), C.c_uint64(seed), int(kmeans_iters),
+                                                out.ctypes.data_as(C.POINTER(C.c_int32)) if want_labels else None),
+                    "cfust_init_partitions")
+        return out
+
+    def init_select(self, m: int, labels=None, burn_in: int = 0):
+        """Alg. 1 steps 2-12 (readings I3, I4): (loglik0[m], best); installs the winner's Psi."""
+        ll = np.zeros(m)
+        best = C.c_int32(-1)
+        lab = None
+        if labels is not None:
+            lab = np.ascontiguousarray(np.asarray(labels, dtype=np.int32))
+            assert lab.shape == (m, self.n)
+        self._check(lib().cfust_init_select(self._ctx, int(m), lab.ctypes.data_as(C.POINTER(C.c_int32))
+                                            if lab is not None else None, int(burn_in), _dptr(ll), C.byref(best)),
+                    "cfust_init_select")
+        return ll, int(best.value)
 
     def timing(self, reset: bool = False):
         ms = np.zeros(4)

@@ -30,7 +30,7 @@ class Opts(C.Structure):
                 ("lattice_shift", C.POINTER(C.c_double)), ("nu_lo", C.c_double), ("nu_hi", C.c_double),
                 ("y_on_device", C.c_int32), ("device", C.c_int32), ("rank", C.c_int32), ("world", C.c_int32),
                 ("nccl_id", C.c_void_p), ("n_total", C.c_int64), ("timing", C.c_int32),
-                ("e1_exact", C.c_int32)]
+                ("e1_exact", C.c_int32), ("global_offset", C.c_int64)]
 
 
 class Result(C.Structure):
@@ -42,6 +42,7 @@ class Result(C.Structure):
 EXPORTS = ["cfust_em_init", "cfust_set_data", "cfust_estep", "cfust_mstep", "cfust_iterate", "cfust_loglik",
            "cfust_fit", "cfust_get_params", "cfust_set_params", "cfust_get_pairs", "cfust_get_timing",
            "cfust_stream", "cfust_launch_count", "cfust_nccl_unique_id", "cfust_eval_special", "cfust_k_stats",
+           "cfust_init_partitions", "cfust_init_select",
            "cfust_last_error", "cfust_destroy"]
 
 _lib = None
@@ -73,6 +74,9 @@ def lib():
         L.cfust_nccl_unique_id.argtypes = [vp]
         L.cfust_k_stats.argtypes = [i32, i32]
         L.cfust_eval_special.argtypes = [i32, dp, dp, i64, C.c_double]
+        pi32 = C.POINTER(C.c_int32)
+        L.cfust_init_partitions.argtypes = [vp, i32, C.c_uint64, i32, pi32]
+        L.cfust_init_select.argtypes = [vp, i32, pi32, i32, dp, pi32]
         L.cfust_last_error.argtypes = [vp]
         L.cfust_last_error.restype = C.c_char_p
         L.cfust_destroy.argtypes = [vp]

@@ -9,7 +9,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libcfust.so")
-SOURCES = ["cfust_kernels.cu", "cfust_abi.cu"]
+SOURCES = ["cfust_kernels.cu", "cfust_init.cu", "cfust_abi.cu"]
 HEADERS = ["cfust_device.cuh", "cfust_internal.h", "cfust_special.cuh", "cfust_coeffs.h"]
 
 

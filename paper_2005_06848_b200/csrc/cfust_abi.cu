@@ -33,6 +33,13 @@ struct cfust_ctx {
     int64_t counts[4] = {0, 0, 0, 0};
     int64_t launches = 0;
     int nblocks_last = 0;
+    int64_t j0 = 0;                // global index of the first local observation
+    // Alg. 1 workspace (allocated on first use)
+    int32_t *d_labels = nullptr;   // [m_cap][n]
+    int m_cap = 0;
+    double *d_init = nullptr;      // mind[n] | cent[g p] | ybar[g p] | sums1 | sums2 | argmax scratch
+    int *d_iflag = nullptr;        // [GMAX + 1]: empty flags, valid
+    double *h_ipin = nullptr;      // pinned staging for Alg. 1 scalars
     std::string err;
 };
 
@@ -205,6 +212,10 @@ void cfust_destroy(cfust_ctx *ctx) {
     cudaFree(s.stats);
     cudaFree(s.status);
     cudaFree(ctx->d_ll);
+    cudaFree(ctx->d_labels);
+    cudaFree(ctx->d_init);
+    cudaFree(ctx->d_iflag);
+    cudaFreeHost(ctx->h_ipin);
     cudaFreeHost(ctx->h_pin);
     cudaFreeHost(ctx->h_status);
     for (auto &e : ctx->ev)
@@ -246,6 +257,7 @@ int cfust_em_init(cfust_ctx **out, const double *y, int64_t n, int32_t p, int32_
         if (rc != CFUST_OK) break;
         ctx->world = opts->world > 1 ? opts->world : 1;
         ctx->rank = opts->rank;
+        ctx->j0 = opts->global_offset > 0 ? opts->global_offset : 0;
         ctx->timing = opts->timing != 0;
         int ndev = 0;
         if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev < 1) { rc = fail(ctx, CFUST_ECUDA, "no CUDA device"); break; }
@@ -536,6 +548,254 @@ int cfust_eval_special(int32_t which, const double *x, double *y, int64_t n, dou
     cudaFree(dx);
     cudaFree(dy);
     return rc;
+}
+
+// ------------------------------------------------------------------------------------------
+// Alg. 1: parallel multi-start initialisation, readings I1-I4.
+namespace {
+
+struct InitWS {
+    double *mind, *cent, *ybar, *sums1, *sums2, *scratch, *amax, *gath;
+};
+
+constexpr int SCRATCH = 2048 + 2;
+
+InitWS init_ws(cfust_ctx *ctx) {
+    const DevState &s = ctx->s;
+    InitWS w;
+    w.mind = ctx->d_init;
+    w.cent = w.mind + (s.n > 0 ? s.n : 1);
+    w.ybar = w.cent + GMAX * PMAX;
+    w.sums1 = w.ybar + GMAX * PMAX;
+    w.sums2 = w.sums1 + GMAX * (PMAX + 1);
+    w.scratch = w.sums2 + GMAX * (PMAX * (PMAX + 1) / 2 + PMAX);
+    w.amax = w.scratch + 2048;
+    w.gath = w.amax + 2;
+    return w;
+}
+
+int ensure_init_ws(cfust_ctx *ctx, int m) {
+    const DevState &s = ctx->s;
+    if (!ctx->d_init) {
+        const size_t len = size_t(s.n > 0 ? s.n : 1) + 2 * GMAX * PMAX + GMAX * (PMAX + 1) +
+                           GMAX * (PMAX * (PMAX + 1) / 2 + PMAX) + SCRATCH + 2 * size_t(ctx->world);
+        CU(cudaMalloc((void **)&ctx->d_init, sizeof(double) * len));
+        CU(cudaMalloc((void **)&ctx->d_iflag, sizeof(int) * (GMAX + 1)));
+        CU(cudaMallocHost((void **)&ctx->h_ipin, sizeof(double) * (64 + 2 * size_t(ctx->world))));
+    }
+    if (m > ctx->m_cap) {
+        cudaFree(ctx->d_labels);
+        ctx->d_labels = nullptr;
+        CU(cudaMalloc((void **)&ctx->d_labels, sizeof(int32_t) * size_t(m) * (s.n > 0 ? s.n : 1)));
+        ctx->m_cap = m;
+    }
+    return CFUST_OK;
+}
+
+int sync_ctx(cfust_ctx *ctx) {
+    CU(cudaStreamSynchronize(ctx->stream));
+    return CFUST_OK;
+}
+
+int allreduce_sum(cfust_ctx *ctx, double *buf, size_t len) {
+    if (ctx->world > 1) NC(ncclAllReduce(buf, buf, len, ncclDouble, ncclSum, ctx->comm, ctx->stream));
+    return CFUST_OK;
+}
+
+// global per-component sums over labels `lab` (pass 1 or 2) into out (device), all ranks
+int global_part_sums(cfust_ctx *ctx, const int32_t *lab, const double *ybar, int pass, double *out) {
+    const DevState &s = ctx->s;
+    const int E = part_sums_width(s.p, s.g, pass);
+    const int cap = int(size_t(max_partial_blocks(s)) * (size_t(s.g) * s.K + 1) / size_t(E));
+    int nb = 0;
+    CUI(launch_part_sums(s.y, s.n, s.p, s.g, lab, ybar, pass, cap < 4 * s.num_sms ? cap : 4 * s.num_sms, s.partials, &nb,
+                         ctx->stream));
+    CUI(launch_reduce_cols(s.partials, nb, E, E, out, ctx->stream));
+    ctx->launches += 2;
+    return allreduce_sum(ctx, out, size_t(E));
+}
+
+// global argmax of w.mind (ties -> lowest global index) -> (*val, *idx) on the host
+int global_argmax(cfust_ctx *ctx, const InitWS &w, double *val, int64_t *idx) {
+    const DevState &s = ctx->s;
+    CUI(launch_argmax(w.mind, s.n, ctx->j0, w.scratch, w.amax, ctx->stream));
+    ctx->launches += 2;
+    if (ctx->world > 1) {
+        NC(ncclAllGather(w.amax, w.gath, 2, ncclDouble, ctx->comm, ctx->stream));
+        CU(cudaMemcpyAsync(ctx->h_ipin, w.gath, sizeof(double) * 2 * ctx->world, cudaMemcpyDeviceToHost, ctx->stream));
+    } else {
+        CU(cudaMemcpyAsync(ctx->h_ipin, w.amax, sizeof(double) * 2, cudaMemcpyDeviceToHost, ctx->stream));
+    }
+    int rc = sync_ctx(ctx);
+    if (rc) return rc;
+    double bv = -1.0;
+    int64_t bi = INT64_MAX;
+    for (int r = 0; r < ctx->world; ++r) {
+        const double v = ctx->h_ipin[2 * r];
+        const int64_t i = int64_t(ctx->h_ipin[2 * r + 1]);
+        if (v > bv || (v == bv && i < bi)) { bv = v; bi = i; }
+    }
+    *val = bv;
+    *idx = bi;
+    return CFUST_OK;
+}
+
+// centre slot k <- y_{jg} (global index), broadcast from its owner; mind[jg] <- 0 if set_zero
+int set_center_from_point(cfust_ctx *ctx, const InitWS &w, int k, int64_t jg, bool zero_mind) {
+    const DevState &s = ctx->s;
+    double *dst = w.cent + size_t(k) * s.p;
+    const bool mine = jg >= ctx->j0 && jg < ctx->j0 + s.n;
+    if (mine) {
+        CU(cudaMemcpyAsync(dst, s.y + (jg - ctx->j0) * s.p, sizeof(double) * s.p, cudaMemcpyDeviceToDevice, ctx->stream));
+        if (zero_mind) CU(cudaMemsetAsync(w.mind + (jg - ctx->j0), 0, sizeof(double), ctx->stream));
+    } else {
+        CU(cudaMemsetAsync(dst, 0, sizeof(double) * s.p, ctx->stream));
+    }
+    return allreduce_sum(ctx, dst, size_t(s.p));   // exactly one rank contributes non-zeros
+}
+
+uint64_t splitmix64_host(uint64_t x) {
+    uint64_t z = x + 0x9E3779B97F4A7C15ULL;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+    return z ^ (z >> 31);
+}
+
+int kmeans_partition(cfust_ctx *ctx, uint64_t seed, int iters, int32_t *lab) {
+    const DevState &s = ctx->s;
+    const InitWS w = init_ws(ctx);
+    const int64_t nt = int64_t(s.n_total);
+    const int64_t jstar = int64_t(splitmix64_host(seed ^ 0xA5A5A5A5A5A5A5A5ULL) % uint64_t(nt));
+    int rc = set_center_from_point(ctx, w, 0, jstar, false);
+    if (rc) return rc;
+    CUI(launch_mind(s.y, s.n, s.p, w.cent, w.mind, 1, ctx->stream));
+    ctx->launches += 1;
+    for (int k = 1; k < s.g; ++k) {   // farthest point (reading I2)
+        double v;
+        int64_t jb;
+        if ((rc = global_argmax(ctx, w, &v, &jb))) return rc;
+        if ((rc = set_center_from_point(ctx, w, k, jb, false))) return rc;
+        CUI(launch_mind(s.y, s.n, s.p, w.cent + size_t(k) * s.p, w.mind, 0, ctx->stream));
+        ctx->launches += 1;
+    }
+    CU(cudaMemsetAsync(lab, 0xFF, sizeof(int32_t) * (s.n > 0 ? s.n : 1), ctx->stream));   // labels -1
+    for (int it = 0; it < iters; ++it) {
+        int nb = 0;
+        CUI(launch_assign(s.y, s.n, s.p, s.g, w.cent, lab, w.mind, s.partials, &nb, ctx->stream));
+        CUI(launch_reduce_cols(s.partials, nb, 1, 1, w.amax, ctx->stream));
+        ctx->launches += 2;
+        if ((rc = allreduce_sum(ctx, w.amax, 1))) return rc;
+        CU(cudaMemcpyAsync(ctx->h_ipin, w.amax, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+        if ((rc = sync_ctx(ctx))) return rc;
+        if (ctx->h_ipin[0] == 0.0) break;
+        if ((rc = global_part_sums(ctx, lab, nullptr, 1, w.sums1))) return rc;
+        CUI(launch_centers(w.sums1, s.p, s.g, w.cent, ctx->d_iflag, ctx->stream));
+        ctx->launches += 1;
+        int hflag[GMAX];
+        CU(cudaMemcpyAsync(hflag, ctx->d_iflag, sizeof(int) * s.g, cudaMemcpyDeviceToHost, ctx->stream));
+        if ((rc = sync_ctx(ctx))) return rc;
+        for (int i = 0; i < s.g; ++i) {   // empty cluster: re-seed to the farthest point
+            if (!hflag[i]) continue;
+            double v;
+            int64_t jb;
+            if ((rc = global_argmax(ctx, w, &v, &jb))) return rc;
+            if ((rc = set_center_from_point(ctx, w, i, jb, true))) return rc;
+        }
+    }
+    return CFUST_OK;
+}
+
+int random_partition(cfust_ctx *ctx, uint64_t seed, int l, int m, int32_t *lab) {
+    const DevState &s = ctx->s;
+    const InitWS w = init_ws(ctx);
+    for (int attempt = 0; attempt < 1000; ++attempt) {
+        CUI(launch_random_labels(lab, s.n, ctx->j0, s.g, seed, int64_t(l) + int64_t(m) * attempt, ctx->stream));
+        ctx->launches += 1;
+        int rc = global_part_sums(ctx, lab, nullptr, 1, w.sums1);
+        if (rc) return rc;
+        CU(cudaMemcpyAsync(ctx->h_ipin, w.sums1, sizeof(double) * s.g * (1 + s.p), cudaMemcpyDeviceToHost, ctx->stream));
+        if ((rc = sync_ctx(ctx))) return rc;
+        bool ok = true;
+        for (int i = 0; i < s.g; ++i)
+            if (ctx->h_ipin[i * (1 + s.p)] < double(s.p + 1)) ok = false;
+        if (ok) return CFUST_OK;
+    }
+    return fail(ctx, CFUST_EINVAL, "no random partition with >= p+1 members per component in 1000 draws");
+}
+
+}  // namespace
+
+int cfust_init_partitions(cfust_ctx *ctx, int32_t m, uint64_t seed, int32_t kmeans_iters, int32_t *labels_out) {
+    if (!ctx || m < 1 || kmeans_iters < 0) return CFUST_EINVAL;
+    DevState &s = ctx->s;
+    if (s.n_total < double(s.g)) return fail(ctx, CFUST_EINVAL, "n_total < g");
+    CU(cudaSetDevice(ctx->device));
+    int rc = ensure_init_ws(ctx, m);
+    if (rc) return rc;
+    const size_t nn = size_t(s.n > 0 ? s.n : 1);
+    rc = kmeans_partition(ctx, seed, kmeans_iters, ctx->d_labels);
+    for (int l = 1; l < m && !rc; ++l) rc = random_partition(ctx, seed, l, m, ctx->d_labels + size_t(l) * nn);
+    if (rc) return rc;
+    if (labels_out && s.n > 0)
+        CU(cudaMemcpyAsync(labels_out, ctx->d_labels, sizeof(int32_t) * size_t(m) * s.n, cudaMemcpyDeviceToHost,
+                           ctx->stream));
+    return sync_ctx(ctx);
+}
+
+int cfust_init_select(cfust_ctx *ctx, int32_t m, const int32_t *labels, int32_t burn_in, double *loglik0_out,
+                      int32_t *best_out) {
+    if (!ctx || m < 1 || burn_in < 0) return CFUST_EINVAL;
+    DevState &s = ctx->s;
+    if (!labels && m > ctx->m_cap) return fail(ctx, CFUST_EINVAL, "no partitions: call cfust_init_partitions first");
+    CU(cudaSetDevice(ctx->device));
+    int rc = ensure_init_ws(ctx, m);
+    if (rc) return rc;
+    const size_t nn = size_t(s.n > 0 ? s.n : 1);
+    if (labels && s.n > 0)
+        CU(cudaMemcpyAsync(ctx->d_labels, labels, sizeof(int32_t) * size_t(m) * s.n, cudaMemcpyHostToDevice, ctx->stream));
+    const InitWS w = init_ws(ctx);
+    const int p = s.p, q = s.q, g = s.g;
+    std::vector<double> bp(size_t(g) * (1 + p + p * p + p * (q > 0 ? q : 1) + 1));
+    cfust_params best_params{bp.data(), bp.data() + g, bp.data() + g + g * p, bp.data() + g + g * p + g * p * p,
+                             bp.data() + g + g * p + g * p * p + g * p * (q > 0 ? q : 1)};
+    int best = -1;
+    double best_ll = -INFINITY;
+    for (int c = 0; c < m; ++c) {
+        double ll = -INFINITY;
+        const int32_t *lab = ctx->d_labels + size_t(c) * nn;
+        // Psi^(0) from the partition moments (reading I3), on the device
+        if ((rc = global_part_sums(ctx, lab, nullptr, 1, w.sums1))) return rc;
+        CUI(launch_centers(w.sums1, p, g, w.ybar, ctx->d_iflag, ctx->stream));
+        if ((rc = global_part_sums(ctx, lab, w.ybar, 2, w.sums2))) return rc;
+        const int one = 1;
+        CU(cudaMemcpyAsync(ctx->d_iflag + GMAX, &one, sizeof(int), cudaMemcpyHostToDevice, ctx->stream));
+        if ((rc = reset_status(ctx))) return rc;
+        CUI(launch_partition_params(s, w.sums1, w.sums2, w.ybar, ctx->d_iflag + GMAX, ctx->stream));
+        int valid = 0;
+        CU(cudaMemcpyAsync(&valid, ctx->d_iflag + GMAX, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+        if ((rc = sync_ctx(ctx))) return rc;
+        ctx->launches += 2;
+        if (valid) {
+            CUI(launch_derive(s, ctx->stream));
+            CUI(launch_chi(s, ctx->stream));
+            ctx->launches += 2;
+            int r2 = fetch_status_and_sync(ctx);
+            for (int it = 0; it < burn_in && r2 == CFUST_OK; ++it) r2 = cfust_iterate(ctx, nullptr);
+            if (r2 == CFUST_OK) r2 = cfust_loglik(ctx, &ll);
+            if (r2 == CFUST_ECUDA || r2 == CFUST_ENCCL) return r2;
+            if (r2 != CFUST_OK) ll = -INFINITY;   // candidate failed (ENOTPD, EUNDERFLOW, EEMPTY): skipped
+        }
+        if (loglik0_out) loglik0_out[c] = ll;
+        if (ll > best_ll) {   // strict: ties keep the lowest index (reading I4)
+            best_ll = ll;
+            best = c;
+            if ((rc = cfust_get_params(ctx, &best_params))) return rc;
+        }
+    }
+    if (best < 0) return fail(ctx, CFUST_EINVAL, "every initial partition is invalid");
+    if (best_out) *best_out = best;
+    ctx->err.clear();
+    return cfust_set_params(ctx, &best_params);
 }
 
 int cfust_get_timing(cfust_ctx *ctx, double *ms, int64_t *counts, int32_t reset) {

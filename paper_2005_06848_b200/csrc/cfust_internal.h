@@ -48,4 +48,18 @@ int upload_special_constants();
 int launch_special(int which, const double *x, double *y, int64_t n, double aux, cudaStream_t st);
 int max_partial_blocks(const DevState &s);
 
+// Alg. 1 (cfust_init.cu)
+int launch_random_labels(int32_t *lab, int64_t n, int64_t j0, int g, uint64_t seed, int64_t stream, cudaStream_t st);
+int launch_mind(const double *y, int64_t n, int p, const double *c, double *mind, int init, cudaStream_t st);
+int launch_argmax(const double *v, int64_t n, int64_t j0, double *scratch, double *out, cudaStream_t st);
+int launch_assign(const double *y, int64_t n, int p, int g, const double *cen, int32_t *lab, double *mind,
+                  double *partials, int *nb_out, cudaStream_t st);
+int part_sums_width(int p, int g, int pass);
+int launch_part_sums(const double *y, int64_t n, int p, int g, const int32_t *lab, const double *ybar, int pass,
+                     int max_blocks, double *partials, int *nb_out, cudaStream_t st);
+int launch_centers(const double *sums1, int p, int g, double *out, int *empty, cudaStream_t st);
+int launch_partition_params(const DevState &s, const double *sums1, const double *sums2, const double *ybar, int *valid,
+                            cudaStream_t st);
+int launch_reduce_cols(const double *partials, int nblocks, int stride, int ncols, double *out, cudaStream_t st);
+
 }  // namespace cfust

@@ -1181,6 +1181,11 @@ int launch_reduce(const DevState &s, int nblocks, int mode, double *out, cudaStr
     return int(cudaGetLastError());
 }
 
+int launch_reduce_cols(const double *partials, int nblocks, int stride, int ncols, double *out, cudaStream_t st) {
+    reduce_kernel<<<(ncols + 127) / 128, 128, 0, st>>>(partials, nblocks, stride, 0, ncols, out);
+    return int(cudaGetLastError());
+}
+
 int launch_mstep(const DevState &s, cudaStream_t st) {
     mstep_kernel<<<1, 32, 0, st>>>(s);
     return int(cudaGetLastError());
