@@ -4,8 +4,9 @@
 //                               components; the M lattice points of every T_r are split
 //                               over the 32 lanes and combined by xor-shuffle reductions
 //                               (Alg. 2; formulas DESIGN.md §3).
-//   estep_t_kernel              q == 0 (Delta = 0): one thread per
-//                               (observation, component), tiles of 32 observations.
+//   estep_t_mma_kernel<G>       q == 0 (Delta = 0): warp per 32 observations,
+//                               S3 by FP64 tensor-core MMA (default); estep_t_kernel<P> is the
+//                               shared-memory register-blocked variant (CFUST_T_MMA=0).
 //   reduce_kernel               deterministic second pass over per-block partial sums.
 //   mstep_kernel                per-component M-step (Alg. 3; reading R-M).
 //   derive_kernel               Omega, chol, A, Lambda, constants.
@@ -743,6 +744,144 @@ __global__ void __launch_bounds__(TT, 2) estep_t_kernel(EArgs A, int mode) {
 }
 
 // ------------------------------------------------------------------------------------------
+// q == 0, FP64-tensor-core variant (default): one warp per tile of 32 observations, no block
+// barriers in the main loop.  Phase 1 (lane = observation): d, log f, tau, e2, e1-e2 for all G
+// components with branch-free special functions; S0, S1, S7 accumulate per lane.  Phase 2 (warp):
+// S3_i += sum_j w_ij y_j y_j' (w = tau e2) as DMMA m8n8k4: per group of 4 observations lane
+// (m = lane>>2, k = lane&3) supplies a = w_{j_k} y_{j_k,m} and b = y_{j_k,m} (B's element (k, n=m)
+// is the same number), so the 8x8 accumulator fragment of lane holds S3[m][2(lane&3) + {0,1}];
+// S2_i[m] accumulates the same a.  Coordinates m >= p are zero padding.  DMMA runs on the FP64
+// pipe (tools/bench_dmma.cu: 37 TFLOP/s alone, shared with DFMA) — the gain is issue slots: 8
+// instructions per component per 32 observations instead of ~370 FFMA/LDS per observation.
+#ifndef CFUST_T_MMA
+#define CFUST_T_MMA 1
+#endif
+constexpr int TW = 8;   // warps per block of the q = 0 kernel
+#ifndef CFUST_T_MB
+#define CFUST_T_MB 2        // blocks per SM (G = 5 spills ~300 B but runs 15% faster than 1 block, profiles/r01_cfg3_mma.log)
+#endif
+
+__device__ __forceinline__ void dmma_884(double &c0, double &c1, double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                 : "+d"(c0), "+d"(c1)
+                 : "d"(a), "d"(b));
+}
+
+template <int G>
+__global__ void __launch_bounds__(TW * 32, CFUST_T_MB) estep_t_mma_kernel(EArgs A, int mode) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int p = A.p, K = A.K, GK = G * K;
+    CompDev *comp = reinterpret_cast<CompDev *>(smem_raw);
+    double *red = reinterpret_cast<double *>(comp + G);   // [TW][GK + 1]
+    for (int t = threadIdx.x; t < G * int(sizeof(CompDev) / sizeof(double)); t += blockDim.x)
+        reinterpret_cast<double *>(comp)[t] = reinterpret_cast<const double *>(A.comp)[t];
+    for (int t = threadIdx.x; t < TW * (GK + 1); t += blockDim.x) red[t] = 0.0;
+    __syncthreads();
+    double s0[G], s1[G], s7[G], s2[G], c0[G], c1[G];
+#pragma unroll
+    for (int i = 0; i < G; ++i) s0[i] = s1[i] = s7[i] = s2[i] = c0[i] = c1[i] = 0.0;
+    double ll = 0.0;
+    const int cm = lane >> 2, ck = lane & 3;
+    const int64_t n = A.n;
+    const int64_t ntiles = (n + 31) / 32;
+    for (int64_t tile = int64_t(blockIdx.x) * TW + wid; tile < ntiles; tile += int64_t(gridDim.x) * TW) {
+        const int64_t j = tile * 32 + lane;
+        const bool valid = j < n;
+        double y[PMAX];
+#pragma unroll
+        for (int a = 0; a < PMAX; ++a) y[a] = (valid && a < p) ? __ldg(A.y + j * p + a) : 0.0;
+        double lf[G], dd[G], l1[G];
+        double mx = -CUDART_INF;
+#pragma unroll
+        for (int i = 0; i < G; ++i) {
+            const CompDev &cp = comp[i];
+            double v[PMAX], d = 0.0;
+#pragma unroll
+            for (int a = 0; a < PMAX; ++a) {
+                if (a < p) {
+                    double t = y[a] - cp.mu[a];
+#pragma unroll
+                    for (int b = 0; b < a; ++b) t = fma(-cp.L[a * PMAX + b], v[b], t);
+                    v[a] = t * cp.Linv[a];
+                    d = fma(v[a], v[a], d);
+                }
+            }
+            dd[i] = d;
+            l1[i] = log1p_pos(d * cp.inv_nu);
+            lf[i] = cp.logpi + cp.kappa - 0.5 * cp.m0 * l1[i];
+            mx = fmax(mx, lf[i]);
+        }
+        double se = 0.0;
+#pragma unroll
+        for (int i = 0; i < G; ++i) { lf[i] = exp_neg(lf[i] - mx); se += lf[i]; }   // lf <- exp(lf - max)
+        if (valid && mx == -CUDART_INF) atomicOr(A.status, 1);
+        if (valid) ll += mx + log_unit(se);
+        if (mode == 1) continue;
+        const double ise = div_fast(1.0, se);
+        double w[G];
+#pragma unroll
+        for (int i = 0; i < G; ++i) {
+            const CompDev &cp = comp[i];
+            const double tau = valid ? lf[i] * ise : 0.0;
+            const double e2 = div_fast(cp.m0, cp.nu + dd[i]);
+            const double e1me2 = cp.psi_half_m0 - (cp.log_half_nu + l1[i]) - e2;   // log(rho/2) = log(nu/2) + log1p(d/nu)
+            s0[i] += tau;
+            w[i] = tau * e2;
+            s1[i] += w[i];
+            s7[i] = fma(tau, e1me2, s7[i]);
+        }
+        // phase 2: 8 groups of 4 observations
+#pragma unroll 2
+        for (int sg = 0; sg < 8; ++sg) {
+            const int64_t jj = tile * 32 + 4 * sg + ck;
+            const double yv = (cm < p && jj < n) ? __ldg(A.y + jj * p + cm) : 0.0;
+#pragma unroll
+            for (int i = 0; i < G; ++i) {
+                const double a = __shfl_sync(0xffffffffu, w[i], 4 * sg + ck) * yv;
+                s2[i] += a;
+                dmma_884(c0[i], c1[i], a, yv);
+            }
+        }
+    }
+    // ---- warp epilogue -> red[wid][*], then block sum over warps in fixed order
+    double *rw = red + wid * (GK + 1);
+    ll = warp_sum(ll);
+    if (lane == 0) rw[GK] = ll;
+    if (mode != 1) {
+        const int S3o = 2 + p;   // offsets inside a component's K entries
+#pragma unroll
+        for (int i = 0; i < G; ++i) {
+            const double t0 = warp_sum(s0[i]), t1 = warp_sum(s1[i]), t7 = warp_sum(s7[i]);
+            double a2 = s2[i];
+            a2 += __shfl_xor_sync(0xffffffffu, a2, 1);
+            a2 += __shfl_xor_sync(0xffffffffu, a2, 2);
+            double *ri = rw + i * K;
+            if (lane == 0) { ri[0] = t0; ri[1] = t1; ri[K - 1] = t7; }
+            if (ck == 0 && cm < p) ri[2 + cm] = a2;
+            // S3 upper, row-major packed: entry (a, b), a <= b
+            const int a = cm;
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int b = 2 * ck + h;
+                if (a < p && b < p && a <= b) {
+                    const int off = a * p - a * (a - 1) / 2 + (b - a);
+                    ri[S3o + off] = h ? c1[i] : c0[i];
+                }
+            }
+        }
+    }
+    __syncthreads();
+    double *out = A.partials + size_t(blockIdx.x) * (GK + 1);
+    for (int e = threadIdx.x; e <= GK; e += blockDim.x) {
+        if (mode == 1 && e != GK) continue;
+        double v = 0.0;
+        for (int wv = 0; wv < TW; ++wv) v += red[wv * (GK + 1) + e];
+        out[e] = v;
+    }
+}
+
+// ------------------------------------------------------------------------------------------
 __global__ void reduce_kernel(const double *__restrict__ partials, int nblocks, int stride, int col0, int ncols,
                               double *__restrict__ out) {
     for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < ncols; e += gridDim.x * blockDim.x) {
@@ -1104,6 +1243,40 @@ static int launch_cfust_mode(const DevState &s, EArgs &a, cudaStream_t st, int *
     }
 }
 
+template <int G>
+static int launch_t_mma_g(const DevState &s, EArgs &a, int mode, cudaStream_t st, int *nb) {
+    auto kern = estep_t_mma_kernel<G>;
+    const size_t sm = sizeof(CompDev) * G + sizeof(double) * TW * (size_t(G) * s.K + 1);
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
+    if (e != cudaSuccess) return int(e);
+    int per_sm = 0;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, TW * 32, sm);
+    if (e != cudaSuccess) return int(e);
+    if (per_sm < 1) per_sm = 1;
+    const int64_t ntiles = (a.n + 31) / 32;
+    int64_t blocks = int64_t(s.num_sms) * per_sm;
+    const int64_t need = (ntiles + TW - 1) / TW;
+    if (blocks > need) blocks = need;
+    if (blocks < 1) blocks = 1;
+    kern<<<int(blocks), TW * 32, sm, st>>>(a, mode);
+    *nb = int(blocks);
+    return int(cudaGetLastError());
+}
+
+static int launch_t_mma(const DevState &s, EArgs &a, int mode, cudaStream_t st, int *nb) {
+    switch (s.g) {
+        case 1: return launch_t_mma_g<1>(s, a, mode, st, nb);
+        case 2: return launch_t_mma_g<2>(s, a, mode, st, nb);
+        case 3: return launch_t_mma_g<3>(s, a, mode, st, nb);
+        case 4: return launch_t_mma_g<4>(s, a, mode, st, nb);
+        case 5: return launch_t_mma_g<5>(s, a, mode, st, nb);
+        case 6: return launch_t_mma_g<6>(s, a, mode, st, nb);
+        case 7: return launch_t_mma_g<7>(s, a, mode, st, nb);
+        case 8: return launch_t_mma_g<8>(s, a, mode, st, nb);
+        default: return int(cudaErrorInvalidValue);
+    }
+}
+
 template <int P>
 static int launch_t_p(const DevState &s, EArgs &a, int mode, cudaStream_t st, int *nb) {
     auto kern = estep_t_kernel<P>;
@@ -1152,6 +1325,7 @@ int launch_estep(const DevState &s, int mode, const int64_t *idx, int64_t cnt, d
             dump_t_kernel<<<int(blocks > 4096 ? 4096 : blocks), 128, 0, st>>>(a);
             return int(cudaGetLastError());
         }
+        if (CFUST_T_MMA) return launch_t_mma(s, a, mode, st, nblocks_out);
         switch (s.p) {
             case 1: return launch_t_p<1>(s, a, mode, st, nblocks_out);
             case 2: return launch_t_p<2>(s, a, mode, st, nblocks_out);

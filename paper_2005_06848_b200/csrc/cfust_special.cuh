@@ -79,7 +79,7 @@ __device__ __forceinline__ double exp_neg(double x) {
 #endif
 }
 
-// log(x) for normal x in (0, 1]: x = m 2^e, m in [sqrt(1/2), sqrt(2)); log m = 2 atanh(s),
+// log(x) for normal x > 0: x = m 2^e, m in [sqrt(1/2), sqrt(2)); log m = 2 atanh(s),
 // s = (m-1)/(m+1) (m-1 exact), series to s^21.  Relative accuracy holds as x -> 1 (e = 0).
 __device__ __forceinline__ double log_unit(double x) {
 #if CFUST_OWN_ELEM
@@ -97,6 +97,15 @@ __device__ __forceinline__ double log_unit(double x) {
 #else
     return log(x);
 #endif
+}
+
+// log(1 + x), x >= 0: log of z = 1 + x (log_unit handles any positive normal z) plus the
+// rounding correction (x - (z - 1)) / z (a tiny term: an approximate reciprocal suffices).
+__device__ __forceinline__ double log1p_pos(double x) {
+    const double z = 1.0 + x;
+    double r;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(z));
+    return fma(x - (z - 1.0), r, log_unit(z));
 }
 
 // sqrt(w), w >= 0 finite: rsqrt seed + two Newton steps + one residual correction.
