@@ -18,6 +18,12 @@ _SRC = os.path.join(_HERE, "cfust_oracle.c")
 _LIB = os.path.join(_HERE, "libcfust_oracle.so")
 
 OK, EINVAL, ENOTPD, EUNDERFLOW, EEMPTY = 0, -1, -4, -5, -6
+E1_EXACT, FAMILY_SN = 1, 2          # E-step / fit flags (reading R2'; skew-normal family, reading F1)
+FAMILIES = {"st": 0, "sn": FAMILY_SN}   # CFUST (skew-t, default) / CFUSN (skew-normal, nu = inf)
+
+
+def _flags(e1_exact=False, family="st"):
+    return (E1_EXACT if e1_exact else 0) | FAMILIES[family]
 
 
 def build(force: bool = False) -> str:
@@ -77,7 +83,9 @@ def lib():
         L.orc_estep.argtypes = [_I64, _I, _I, _I, _PD, _PD, _PD, _PD, _PD, _PD, C.POINTER(_Lattice),
                                 _I, _I, _PD, _PD, _PD, _PD]
         L.orc_mstep.restype = _I
-        L.orc_mstep.argtypes = [_I, _I, _I, _D, _PD, _PD, _PD, _PD, _PD, _PD, _D, _D]
+        L.orc_mstep.argtypes = [_I, _I, _I, _D, _PD, _PD, _PD, _PD, _PD, _PD, _D, _D, _I]
+        L.orc_pair_sn.restype = _I
+        L.orc_pair_sn.argtypes = [_I, _I, _PD, _PD, _PD, _PD, _PD, _D, C.POINTER(_Lattice), _PD, _PD, _PD]
         L.orc_aitken_stop.restype = _I
         L.orc_aitken_stop.argtypes = [_D, _D, _D, _D]
         L.orc_fit.restype = _I
@@ -98,7 +106,7 @@ def lib():
         L.orc_partition_params.restype = _I
         L.orc_partition_params.argtypes = [_I64, _I, _I, _I, _PD, _PI32, _D, _PD, _PD, _PD, _PD, _PD]
         L.orc_init_select.restype = _I
-        L.orc_init_select.argtypes = [_I64, _I, _I, _I, _PD, _I, _PI32, C.POINTER(_Lattice), _I, _I, _PD,
+        L.orc_init_select.argtypes = [_I64, _I, _I, _I, _PD, _I, _PI32, C.POINTER(_Lattice), _I, _I, _I, _PD,
                                       C.POINTER(_I), _PD, _PD, _PD, _PD, _PD]
     return _lib
 
@@ -188,9 +196,10 @@ def derive(sigma, delta, nu):
     return rc, {"L": L, "A": A[:q], "Lambda": Lam[:q, :q], "logdet": ld[0], "kappa": ka[0]}
 
 
-def pair(y, mu, sigma, delta, nu, lat: Lattice | None, e1_exact: bool = False):
+def pair(y, mu, sigma, delta, nu, lat: Lattice | None, e1_exact: bool = False, family: str = "st"):
     """One (observation, component) pair: dict(logf_noprior, e1me2, e2, e3, e4).
-    e1_exact: e1 = E[log W | y] on T0's lattice points (reading R2') instead of reading A5."""
+    e1_exact: e1 = E[log W | y] on T0's lattice points (reading R2') instead of reading A5.
+    family "sn": the skew-normal limit (CFUSN, nu = inf; reading F1); nu is ignored."""
     y = _f64(y); mu = _f64(mu); p = len(y)
     delta = _f64(delta).reshape(p, -1); q = delta.shape[1]
     rc, dv = derive(sigma, delta, nu)
@@ -203,6 +212,13 @@ def pair(y, mu, sigma, delta, nu, lat: Lattice | None, e1_exact: bool = False):
     gap = np.array([np.inf])
     A = _f64(dv["A"]) if q else np.zeros(1)
     Lam = _f64(dv["Lambda"]) if q else np.zeros(1)
+    if family == "sn":
+        ones = np.ones(lat.M if (lat is not None and q >= 2) else 1)
+        rc = lib().orc_pair_sn(p, q, _p(y), _p(mu), _p(dv["L"]), _p(A), _p(Lam), float(dv["logdet"]),
+                               lat.ptr if lat is not None else None, _p(ones), _p(out), _p(gap))
+        assert rc == OK, rc
+        return {"logf": out[0], "e1me2": out[1], "e2": out[2], "e3": out[3:3 + q],
+                "e4": out[3 + q:].reshape(q, q), "gap": gap[0]}
     rc = lib().orc_pair(p, q, _p(y), _p(mu), _p(dv["L"]), _p(A), _p(Lam), float(nu), float(dv["kappa"]),
                         lat.ptr if lat is not None else None, _p(tabs[0]), _p(tabs[1]), _p(tabs[2]),
                         _p(lv) if lv is not None else None, _p(out), _p(gap))
@@ -219,7 +235,7 @@ def _params(params: dict, g: int, p: int, q: int):
 
 
 def estep(y, params: dict, q: int, lat: Lattice | None, nthreads=None, pairs=False, gaps=False,
-          e1_exact: bool = False):
+          e1_exact: bool = False, family: str = "st"):
     """Full E-step.  Returns dict(stats [g*K+1], loglik, pairs [n,g,4+q+q*q] optional)."""
     y = _f64(y)
     n, p = y.shape
@@ -231,7 +247,7 @@ def estep(y, params: dict, q: int, lat: Lattice | None, nthreads=None, pairs=Fal
     po = np.zeros((n, g, 4 + q + q * q)) if pairs else None
     gp = np.full((n, g), np.inf) if gaps else None
     rc = lib().orc_estep(n, p, q, g, _p(y), _p(pi), _p(mu), _p(sg), _p(de), _p(nu),
-                         lat.ptr if lat is not None else None, _nt(nthreads), int(bool(e1_exact)),
+                         lat.ptr if lat is not None else None, _nt(nthreads), _flags(e1_exact, family),
                          _p(po) if pairs else None, _p(stats), _p(ll), _p(gp) if gaps else None)
     out = {"rc": rc, "stats": stats, "loglik": ll[0]}
     if pairs:
@@ -241,19 +257,19 @@ def estep(y, params: dict, q: int, lat: Lattice | None, nthreads=None, pairs=Fal
     return out
 
 
-def mstep(stats, params: dict, p: int, q: int, n_total: float, nu_lo=0.1, nu_hi=1000.0):
+def mstep(stats, params: dict, p: int, q: int, n_total: float, nu_lo=0.1, nu_hi=1000.0, family: str = "st"):
     g = len(params["pi"])
     pi, mu, sg, de, nu = [a.copy() for a in _params(params, g, p, q)]
     st = _f64(stats)
     rc = lib().orc_mstep(p, q, g, float(n_total), _p(st), _p(pi), _p(mu), _p(sg), _p(de), _p(nu),
-                         float(nu_lo), float(nu_hi))
+                         float(nu_lo), float(nu_hi), FAMILIES[family])
     out = {"pi": pi, "mu": mu, "sigma": sg, "delta": de.reshape(g, p, q) if q > 0 else np.zeros((g, p, 0)),
            "nu": nu}
     return rc, out
 
 
 def fit(y, params: dict, q: int, lat: Lattice | None, max_iter: int, tol: float = 0.0,
-        nthreads=None, nu_lo=0.1, nu_hi=1000.0, e1_exact: bool = False):
+        nthreads=None, nu_lo=0.1, nu_hi=1000.0, e1_exact: bool = False, family: str = "st"):
     y = _f64(y)
     n, p = y.shape
     g = len(params["pi"])
@@ -261,7 +277,7 @@ def fit(y, params: dict, q: int, lat: Lattice | None, max_iter: int, tol: float 
     trace = np.zeros(max_iter + 1)
     ni = C.c_int(0); cv = C.c_int(0)
     rc = lib().orc_fit(n, p, q, g, _p(y), _p(pi), _p(mu), _p(sg), _p(de), _p(nu),
-                       lat.ptr if lat is not None else None, _nt(nthreads), int(bool(e1_exact)), int(max_iter),
+                       lat.ptr if lat is not None else None, _nt(nthreads), _flags(e1_exact, family), int(max_iter),
                        float(tol),
                        float(nu_lo), float(nu_hi), _p(trace), C.byref(ni), C.byref(cv))
     params_out = {"pi": pi, "mu": mu, "sigma": sg,
@@ -309,7 +325,8 @@ def partition_params(y, labels, g: int, q: int, n_total=None):
     return rc, out
 
 
-def init_select(y, labels, g: int, q: int, lat: Lattice | None, burn_in: int = 0, nthreads=None):
+def init_select(y, labels, g: int, q: int, lat: Lattice | None, burn_in: int = 0, nthreads=None,
+                family: str = "st"):
     """Alg. 1 lines 3-12 (readings I3, I4): dict(rc, loglik0[m], best, params)."""
     y = _f64(y)
     n, p = y.shape
@@ -320,7 +337,8 @@ def init_select(y, labels, g: int, q: int, lat: Lattice | None, burn_in: int = 0
     out = {"pi": np.zeros(g), "mu": np.zeros((g, p)), "sigma": np.zeros((g, p, p)),
            "delta": np.zeros((g, p, max(q, 1))), "nu": np.zeros(g)}
     rc = lib().orc_init_select(n, p, int(q), int(g), _p(y), int(m), _i32p(lab), lat.ptr if lat is not None else None,
-                               _nt(nthreads), int(burn_in), _p(ll), C.byref(best), _p(out["pi"]), _p(out["mu"]),
+                               _nt(nthreads), FAMILIES[family], int(burn_in), _p(ll), C.byref(best), _p(out["pi"]),
+                               _p(out["mu"]),
                                _p(out["sigma"]), _p(out["delta"]), _p(out["nu"]))
     out["delta"] = out["delta"][:, :, :q].copy() if q > 0 else np.zeros((g, p, 0))
     return {"rc": rc, "loglik0": ll, "best": best.value, "params": out}

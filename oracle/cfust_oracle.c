@@ -544,6 +544,135 @@ int orc_pair(int p, int q, const double *y, const double *mu, const double *L_om
 }
 
 /* =====================================================================================
+ * Skew-normal family (CFUSN, NEXT-3): the nu -> infinity limit of Eq. (2) (
+ * reading F1).  W = 1, so U | y ~ N_q(c, Lambda) restricted to u > 0 and
+ *   f = 2^q phi_p(y; mu, Omega) Phi_q(c; 0, Lambda),  e2 = 1,  e3 = E1 / P,  e4 = E2 / P,
+ * with the truncated-normal moments of X ~ N_q(c, Lambda) on X > 0 (Tallis):
+ *   P = Phi_q(c; Lambda),  E1 = c P + Lambda h,  h_k = phi(0; c_k, Lambda_kk) Phi_{q-1}(c~(k); S~(k)),
+ *   E2 = sym( Lambda (G + P I) + c E1' ),  G_kl = phi_k [ c~(k)_l P~(k) + (S~(k) h(k))_l ],
+ *   h(k)_t = phi(0; c~(k)_t, S~(k)_tt) Phi_{q-2}(c^(k,t); S^(k,t)),
+ * (c~(k), S~(k)) the normal conditional on x_k = 0.  Phi_r is the chi-normal lattice rule of
+ * orc_Tr with every radius node s_l = 1 (the normal SOV on the same lattice coordinates 1..r-1);
+ * Phi_1 is erfc-exact.  out = [log(2^q phi_p P), 0 (no e1 - e2), 1 (e2), e3 (q), e4 (q*q)].
+ * ===================================================================================== */
+static double norm_logpdf0(double loc, double s2) { return -0.5 * loc * loc / s2 - 0.5 * log(2.0 * ORC_PI * s2); }
+
+static double phi_r(int r, const double *b, const double *S, const orc_lattice *L, const double *ones,
+                    double *min_key_gap) {
+    if (r == 0) return 1.0;
+    if (r == 1) return orc_norm_cdf(b[0] / sqrt(S[0]));
+    return tr_core(r, b, S, INFINITY, L, ones, NULL, min_key_gap, NULL);
+}
+
+int orc_pair_sn(int p, int q, const double *y, const double *mu, const double *L_omega,
+                const double *A, const double *Lambda, double logdet, const orc_lattice *L,
+                const double *ones, double *out, double *min_key_gap) {
+    double r[PMAX], v[PMAX];
+    for (int a = 0; a < p; ++a) r[a] = y[a] - mu[a];
+    for (int a = 0; a < p; ++a) {
+        double s = r[a];
+        for (int b = 0; b < a; ++b) s -= L_omega[a * p + b] * v[b];
+        v[a] = s / L_omega[a * p + a];
+    }
+    double d = 0.0;
+    for (int a = 0; a < p; ++a) d += v[a] * v[a];
+    const double logphi = -0.5 * p * log(2.0 * ORC_PI) - 0.5 * logdet - 0.5 * d;
+    out[1] = 0.0;
+    out[2] = 1.0;
+    if (q == 0) { out[0] = logphi; return ORC_OK; }      /* Gaussian component */
+    double c[QMAX];
+    for (int k = 0; k < q; ++k) {
+        double s = 0.0;
+        for (int a = 0; a < p; ++a) s += A[k * p + a] * r[a];
+        c[k] = s;
+    }
+    const double P = phi_r(q, c, Lambda, L, ones, min_key_gap);
+    const int PW = 3 + q + q * q;
+    if (!(P > 0.0)) {
+        out[0] = -INFINITY;
+        for (int k = 3; k < PW; ++k) out[k] = 0.0;
+        return ORC_OK;
+    }
+    const int q1 = q - 1;
+    double phi[QMAX], Tk[QMAX], h[QMAX], ct[QMAX][QMAX], St[QMAX][QMAX * QMAX];
+    int oth[QMAX][QMAX];
+    for (int k = 0; k < q; ++k) {
+        const double skk = Lambda[k * q + k];
+        phi[k] = exp(norm_logpdf0(c[k], skk));
+        Tk[k] = 1.0;
+        if (q >= 2) {
+            int na = 0;
+            for (int t = 0; t < q; ++t) if (t != k) oth[k][na++] = t;
+            for (int a = 0; a < q1; ++a) {
+                const int ia = oth[k][a];
+                ct[k][a] = c[ia] - Lambda[ia * q + k] * c[k] / skk;
+                for (int b = 0; b < q1; ++b) {
+                    const int ib = oth[k][b];
+                    St[k][a * q1 + b] = Lambda[ia * q + ib] - Lambda[ia * q + k] * Lambda[k * q + ib] / skk;
+                }
+            }
+            Tk[k] = phi_r(q1, ct[k], St[k], L, ones, min_key_gap);
+        }
+        h[k] = phi[k] * Tk[k];
+    }
+    double E1[QMAX];
+    for (int a = 0; a < q; ++a) {
+        double s = c[a] * P;
+        for (int k = 0; k < q; ++k) s += Lambda[a * q + k] * h[k];
+        E1[a] = s;
+    }
+    double G[QMAX * QMAX];
+    memset(G, 0, sizeof(G));
+    if (q >= 2) {
+        const int q2 = q - 2;
+        double Tkt[QMAX][QMAX];
+        for (int k = 0; k < q; ++k)
+            for (int t = k + 1; t < q; ++t) {
+                double val = 1.0;
+                if (q2 >= 1) {
+                    int at = -1;
+                    for (int a = 0; a < q1; ++a) if (oth[k][a] == t) at = a;
+                    const double saa = St[k][at * q1 + at];
+                    double ch[QMAX], Sh[QMAX * QMAX];
+                    int rest[QMAX], nr = 0;
+                    for (int a = 0; a < q1; ++a) if (a != at) rest[nr++] = a;
+                    for (int a = 0; a < q2; ++a) {
+                        const int ra = rest[a];
+                        ch[a] = ct[k][ra] - St[k][ra * q1 + at] * ct[k][at] / saa;
+                        for (int b = 0; b < q2; ++b) {
+                            const int rb = rest[b];
+                            Sh[a * q2 + b] = St[k][ra * q1 + rb] - St[k][ra * q1 + at] * St[k][at * q1 + rb] / saa;
+                        }
+                    }
+                    val = phi_r(q2, ch, Sh, L, ones, min_key_gap);
+                }
+                Tkt[k][t] = Tkt[t][k] = val;
+            }
+        for (int k = 0; k < q; ++k) {
+            double hk[QMAX];
+            for (int a = 0; a < q1; ++a) hk[a] = exp(norm_logpdf0(ct[k][a], St[k][a * q1 + a])) * Tkt[k][oth[k][a]];
+            for (int a = 0; a < q1; ++a) {
+                double s = ct[k][a] * Tk[k];
+                for (int b = 0; b < q1; ++b) s += St[k][a * q1 + b] * hk[b];
+                G[k * q + oth[k][a]] = phi[k] * s;
+            }
+        }
+    }
+    double E2[QMAX * QMAX];
+    for (int a = 0; a < q; ++a)
+        for (int b = 0; b < q; ++b) {
+            double s = 0.0;
+            for (int k = 0; k < q; ++k) s += Lambda[a * q + k] * (G[k * q + b] + (k == b ? P : 0.0));
+            E2[a * q + b] = s + c[a] * E1[b];
+        }
+    out[0] = q * log(2.0) + logphi + log(P);
+    for (int a = 0; a < q; ++a) out[3 + a] = E1[a] / P;
+    for (int a = 0; a < q; ++a)
+        for (int b = 0; b < q; ++b) out[3 + q + a * q + b] = 0.5 * (E2[a * q + b] + E2[b * q + a]) / P;
+    return ORC_OK;
+}
+
+/* =====================================================================================
  * E-step over all observations: Eq. (3)-(4), Alg. 2
  * with the sums S0..S7 (reading A4) accumulated in ascending j.
  * ===================================================================================== */
@@ -555,10 +684,11 @@ typedef struct {
 int orc_estep(int64_t n, int p, int q, int g, const double *y,
               const double *pi, const double *mu, const double *sigma,
               const double *delta, const double *nu, const orc_lattice *L,
-              int nthreads, int e1_exact, double *pair_out, double *stats, double *loglik,
+              int nthreads, int flags, double *pair_out, double *stats, double *loglik,
               double *min_key_gap) {
     if (p < 1 || p > PMAX || q < 0 || q > 6 || g < 1 || n < 0) return ORC_EINVAL;
-    const int use_e1 = e1_exact && q >= 1;          /* q = 0: R1 is already exact */
+    const int sn = (flags & ORC_FAMILY_SN) != 0;
+    const int use_e1 = (flags & ORC_E1_EXACT) && q >= 1 && !sn;   /* q = 0: R1 is already exact */
     const int need_lattice = q >= 2 || use_e1;
     if (need_lattice && (L == NULL || L->M < 1 || L->s < (q > 1 ? q : 1))) return ORC_EINVAL;
     comp_derived *cd = (comp_derived *)calloc(g, sizeof(comp_derived));
@@ -571,9 +701,13 @@ int orc_estep(int64_t n, int p, int q, int g, const double *y,
             cd[i].chi0 = (double *)malloc(sizeof(double) * L->M);
             cd[i].chi1 = (double *)malloc(sizeof(double) * L->M);
             cd[i].chi2 = (double *)malloc(sizeof(double) * L->M);
-            orc_chi_table(L, m0, cd[i].chi0);
-            orc_chi_table(L, m0 + 1.0, cd[i].chi1);
-            orc_chi_table(L, m0 + 2.0, cd[i].chi2);
+            if (sn) {                                    /* normal SOV: every radius node = 1 */
+                for (int64_t l = 0; l < L->M; ++l) cd[i].chi0[l] = cd[i].chi1[l] = cd[i].chi2[l] = 1.0;
+            } else {
+                orc_chi_table(L, m0, cd[i].chi0);
+                orc_chi_table(L, m0 + 1.0, cd[i].chi1);
+                orc_chi_table(L, m0 + 2.0, cd[i].chi2);
+            }
             if (use_e1) {
                 cd[i].lv0 = (double *)malloc(sizeof(double) * L->M);
                 orc_logchi_table(L, m0, cd[i].lv0);
@@ -597,9 +731,11 @@ int orc_estep(int64_t n, int p, int q, int g, const double *y,
             const int64_t j = j0 + jj / g;
             const int i = (int)(jj % g);
             double gap = INFINITY;
-            const int r2 = orc_pair(p, q, y + (size_t)j * p, mu + (size_t)i * p, cd[i].L, cd[i].A,
-                                    cd[i].Lam, nu[i], cd[i].kappa, L, cd[i].chi0, cd[i].chi1,
-                                    cd[i].chi2, cd[i].lv0, buf + (size_t)jj * PW, &gap);
+            const int r2 = sn ? orc_pair_sn(p, q, y + (size_t)j * p, mu + (size_t)i * p, cd[i].L, cd[i].A,
+                                            cd[i].Lam, cd[i].logdet, L, cd[i].chi0, buf + (size_t)jj * PW, &gap)
+                              : orc_pair(p, q, y + (size_t)j * p, mu + (size_t)i * p, cd[i].L, cd[i].A,
+                                         cd[i].Lam, nu[i], cd[i].kappa, L, cd[i].chi0, cd[i].chi1,
+                                         cd[i].chi2, cd[i].lv0, buf + (size_t)jj * PW, &gap);
             gaps[jj] = gap;
             if (r2 != ORC_OK) prc = r2;
         }
@@ -669,7 +805,7 @@ static double nu_eq(double nu, double c) { return log(0.5 * nu) - orc_digamma(0.
 
 int orc_mstep(int p, int q, int g, double n_total, const double *stats,
               double *pi, double *mu, double *sigma, double *delta, double *nu,
-              double nu_lo, double nu_hi) {
+              double nu_lo, double nu_hi, int flags) {
     const int K = orc_k_stats(p, q);
     for (int i = 0; i < g; ++i) {
         const double *S = stats + (size_t)i * K;
@@ -725,8 +861,9 @@ int orc_mstep(int p, int q, int g, double n_total, const double *stats,
             for (int a = 0; a < p; ++a) Si[a * p + a] += 1e-8 * md;
             if (chol(p, Si, Lt) != ORC_OK) return ORC_ENOTPD;
         }
-        /* nu: log(nu/2) - psi(nu/2) decreases from +inf to 0 */
+        /* nu: log(nu/2) - psi(nu/2) decreases from +inf to 0; the skew-normal family has no nu */
         const double cst = S7 / S0;
+        if (flags & ORC_FAMILY_SN) continue;
         if (nu_eq(nu_hi, cst) > 0.0) nu[i] = nu_hi;
         else if (nu_eq(nu_lo, cst) < 0.0) nu[i] = nu_lo;
         else {
@@ -763,17 +900,17 @@ int orc_aitken_stop(double l_km2, double l_km1, double l_k, double tol) {
 /* O13: E-step at Psi^(0) gives l^(0); then [M-step, E-step] per iteration. */
 int orc_fit(int64_t n, int p, int q, int g, const double *y, double *pi, double *mu,
             double *sigma, double *delta, double *nu, const orc_lattice *L,
-            int nthreads, int e1_exact, int max_iter, double tol, double nu_lo, double nu_hi,
+            int nthreads, int flags, int max_iter, double tol, double nu_lo, double nu_hi,
             double *trace, int *n_iter, int *converged) {
     const int K = orc_k_stats(p, q);
     double *stats = (double *)malloc(sizeof(double) * ((size_t)g * K + 1));
     *n_iter = 0;
     *converged = 0;
-    int rc = orc_estep(n, p, q, g, y, pi, mu, sigma, delta, nu, L, nthreads, e1_exact, NULL, stats, &trace[0], NULL);
+    int rc = orc_estep(n, p, q, g, y, pi, mu, sigma, delta, nu, L, nthreads, flags, NULL, stats, &trace[0], NULL);
     for (int k = 1; k <= max_iter && rc == ORC_OK; ++k) {
-        rc = orc_mstep(p, q, g, (double)n, stats, pi, mu, sigma, delta, nu, nu_lo, nu_hi);
+        rc = orc_mstep(p, q, g, (double)n, stats, pi, mu, sigma, delta, nu, nu_lo, nu_hi, flags);
         if (rc != ORC_OK) break;
-        rc = orc_estep(n, p, q, g, y, pi, mu, sigma, delta, nu, L, nthreads, e1_exact, NULL, stats, &trace[k], NULL);
+        rc = orc_estep(n, p, q, g, y, pi, mu, sigma, delta, nu, L, nthreads, flags, NULL, stats, &trace[k], NULL);
         if (rc != ORC_OK) break;
         *n_iter = k;
         if (tol > 0.0 && k >= 2 && orc_aitken_stop(trace[k - 2], trace[k - 1], trace[k], tol)) {
@@ -936,7 +1073,7 @@ int orc_partition_params(int64_t n, int p, int q, int g, const double *y, const 
 /* Alg. 1 lines 3-12 for given partitions: Psi^(0) (I3), optional r burn-in EM iterations,
  * l per candidate (-inf when invalid), selection I4.  params_out receive the winner's Psi. */
 int orc_init_select(int64_t n, int p, int q, int g, const double *y, int m, const int32_t *labels,
-                    const orc_lattice *L, int nthreads, int burn_in, double *loglik0, int *best,
+                    const orc_lattice *L, int nthreads, int flags, int burn_in, double *loglik0, int *best,
                     double *pi, double *mu, double *sigma, double *delta, double *nu) {
     double *cp = (double *)malloc(sizeof(double) * (size_t)(g * (1 + p + p * p + p * (q > 0 ? q : 1) + 1)));
     double *bpi = cp, *bmu = bpi + g, *bsg = bmu + (size_t)g * p, *bde = bsg + (size_t)g * p * p;
@@ -950,12 +1087,12 @@ int orc_init_select(int64_t n, int p, int q, int g, const double *y, int m, cons
         if (burn_in > 0) {
             double *trace = (double *)malloc(sizeof(double) * (burn_in + 1));
             int ni = 0, cv = 0;
-            rc = orc_fit(n, p, q, g, y, bpi, bmu, bsg, bde, bnu, L, nthreads, 0, burn_in, 0.0, 0.1, 1000.0,
+            rc = orc_fit(n, p, q, g, y, bpi, bmu, bsg, bde, bnu, L, nthreads, flags, burn_in, 0.0, 0.1, 1000.0,
                          trace, &ni, &cv);
             ll = trace[ni];
             free(trace);
         } else {
-            rc = orc_estep(n, p, q, g, y, bpi, bmu, bsg, bde, bnu, L, nthreads, 0, NULL, NULL, &ll, NULL);
+            rc = orc_estep(n, p, q, g, y, bpi, bmu, bsg, bde, bnu, L, nthreads, flags, NULL, NULL, &ll, NULL);
         }
         if (rc != ORC_OK || !(ll > -INFINITY)) continue;
         loglik0[c] = ll;

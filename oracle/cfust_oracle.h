@@ -23,6 +23,8 @@ extern "C" {
 #endif
 
 enum { ORC_OK = 0, ORC_EINVAL = -1, ORC_ENOTPD = -4, ORC_EUNDERFLOW = -5, ORC_EEMPTY = -6 };
+/* E-step / fit flags: exact e1 (reading R2'); skew-normal family (CFUSN, nu = inf; reading F1) */
+enum { ORC_E1_EXACT = 1, ORC_FAMILY_SN = 2 };
 
 typedef struct {
     int32_t M;            /* number of lattice points (power of two) */
@@ -65,19 +67,24 @@ int orc_pair(int p, int q, const double *y, const double *mu, const double *L_om
              const orc_lattice *L, const double *chi_m0, const double *chi_m1,
              const double *chi_m2, const double *lv_m0, double *out, double *min_key_gap);
 
-/* ---- E-step over n observations (O9-O10); e1_exact: 0 reading A5 (R1), 1 exact (R2') ----
+/* ---- skew-normal pair (CFUSN, reading F1): ones = radius table of 1.0 (normal SOV) ---- */
+int orc_pair_sn(int p, int q, const double *y, const double *mu, const double *L_omega,
+                const double *A, const double *Lambda, double logdet, const orc_lattice *L,
+                const double *ones, double *out, double *min_key_gap);
+
+/* ---- E-step over n observations (O9-O10); flags: ORC_E1_EXACT, ORC_FAMILY_SN ----
  * pair_out (may be NULL): [n][g][4+q+q*q] = logf, tau, e1me2, e2, e3(q), e4(q*q)
  * stats (may be NULL): [g*K + 1], K = 3+p+p(p+1)/2+q+q(q+1)/2+p*q, last entry = loglik */
 int orc_estep(int64_t n, int p, int q, int g, const double *y,
               const double *pi, const double *mu, const double *sigma,
               const double *delta, const double *nu, const orc_lattice *L,
-              int nthreads, int e1_exact, double *pair_out, double *stats, double *loglik,
+              int nthreads, int flags, double *pair_out, double *stats, double *loglik,
               double *min_key_gap);
 
 /* ---- M-step (O11-O12), in place on the parameter arrays ---- */
 int orc_mstep(int p, int q, int g, double n_total, const double *stats,
               double *pi, double *mu, double *sigma, double *delta, double *nu,
-              double nu_lo, double nu_hi);
+              double nu_lo, double nu_hi, int flags);
 
 /* ---- Aitken stopping rule (Alg. 4; reading A8) ---- */
 int orc_aitken_stop(double l_km2, double l_km1, double l_k, double tol);
@@ -85,7 +92,7 @@ int orc_aitken_stop(double l_km2, double l_km1, double l_k, double tol);
 /* ---- fit loop (O13): trace gets loglik^(0..n_iter) ---- */
 int orc_fit(int64_t n, int p, int q, int g, const double *y, double *pi, double *mu,
             double *sigma, double *delta, double *nu, const orc_lattice *L,
-            int nthreads, int e1_exact, int max_iter, double tol, double nu_lo, double nu_hi,
+            int nthreads, int flags, int max_iter, double tol, double nu_lo, double nu_hi,
             double *trace, int *n_iter, int *converged);
 
 int orc_k_stats(int p, int q);
@@ -100,7 +107,7 @@ int orc_kmeans(int64_t n, int p, int g, const double *y, uint64_t seed, int iter
 int orc_partition_params(int64_t n, int p, int q, int g, const double *y, const int32_t *labels,
                          double n_total, double *pi, double *mu, double *sigma, double *delta, double *nu);
 int orc_init_select(int64_t n, int p, int q, int g, const double *y, int m, const int32_t *labels,
-                    const orc_lattice *L, int nthreads, int burn_in, double *loglik0, int *best,
+                    const orc_lattice *L, int nthreads, int flags, int burn_in, double *loglik0, int *best,
                     double *pi, double *mu, double *sigma, double *delta, double *nu);
 
 #ifdef __cplusplus
