@@ -279,6 +279,18 @@ def main():
         next_rows["e1_exact"] = {"estep_ms": x_est, "pairs_per_s": (j1 - j0) * cfg.g / (x_est * 1e-3),
                                  "overhead_vs_default": x_est / (phase_ms[0] / max(1, phase_cnt[0])) - 1.0}
         em_x.close()
+    # skew-normal family (CFUSN, nu = inf; NEXT-3): E-step kernel time on the same workload
+    em_s = cf.CfustEM(yd, cfg.g, cfg.q, init, (M, z, sh), n_total=cfg.n, rank=rank, world=world,
+                      nccl_id=nccl_id_e2e(world, rank, cf, dist) if world > 1 else None, device=local,
+                      timing=True, family="sn")
+    em_s.estep()
+    em_s.timing(reset=True)
+    for _ in range(2):
+        em_s.estep()
+    sms_, scnt = em_s.timing(reset=True)
+    s_est = sms_[0] / max(1, scnt[0])
+    next_rows["skew_normal"] = {"estep_ms": s_est, "pairs_per_s": (j1 - j0) * cfg.g / (s_est * 1e-3)}
+    em_s.close()
     # parallel multi-start initialisation (Alg. 1, NEXT-1): m = 8 candidates (k-means + 7 random),
     # Psi^(0) from partition moments, one density pass each, argmax; wall time on the device stream
     em_i = cf.CfustEM(yd, cfg.g, cfg.q, init, (M, z, sh), n_total=cfg.n, rank=rank, world=world,

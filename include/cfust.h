@@ -71,6 +71,10 @@ typedef struct {
                                       lattice_z[1], lattice_shift[1]); with q = 0 it is a no-op.  */
     int64_t global_offset;         /* global index of this shard's first observation (j0; 0 for one
                                       rank): keys the random partitions and k-means seeding of Alg. 1 */
+    int32_t family;                /* 0: skew-t components (CFUST, Eq. (2)); 1: skew-normal (CFUSN, the
+                                      nu -> inf limit; reading F1): e2 = 1, nu is
+                                      neither used nor updated; with q = 0 a Gaussian mixture
+                                      (PAPER.md:147-151).  NEXT-3. */
 } cfust_opts;
 
 typedef struct {

@@ -58,7 +58,7 @@ class CfustEM:
     def __init__(self, y, g: int, q: int, init: dict, lattice=None, *, n_total: int | None = None,
                  rank: int = 0, world: int = 1, nccl_id: bytes | None = None, device: int = -1,
                  timing: bool = False, nu_lo: float = 0.1, nu_hi: float = 1000.0, e1_exact: bool = False,
-                 global_offset: int = 0):
+                 global_offset: int = 0, family: str = "st"):
         L = lib()
         self._keep = []
         on_dev = hasattr(y, "data_ptr") and getattr(y, "is_cuda", False)
@@ -96,6 +96,7 @@ class CfustEM:
         opts.timing = 1 if timing else 0
         opts.e1_exact = 1 if e1_exact else 0
         opts.global_offset = int(global_offset)
+        opts.family = {"st": 0, "sn": 1}[family]   # skew-t (CFUST) / skew-normal (CFUSN; q = 0: Gaussian)
         ctx = C.c_void_p()
         rc = L.cfust_em_init(C.byref(ctx), yptr, self.n, self.p, self.g, self.q, C.byref(prm), C.byref(opts))
         if rc != 0:

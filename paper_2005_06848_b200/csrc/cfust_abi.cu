@@ -237,7 +237,8 @@ int cfust_em_init(cfust_ctx **out, const double *y, int64_t n, int32_t p, int32_
             break;
         }
         if (n > 0 && !y) { rc = fail(ctx, CFUST_EINVAL, "y is NULL"); break; }
-        const bool use_e1 = opts->e1_exact != 0 && q >= 1;   // q = 0: reading A5 is exact
+        if (opts->family < 0 || opts->family > 1) { rc = fail(ctx, CFUST_EINVAL, "family must be 0 (skew-t) or 1 (skew-normal)"); break; }
+        const bool use_e1 = opts->e1_exact != 0 && q >= 1 && opts->family == 0;   // q = 0: A5 exact; no W for skew-normal
         const bool need_lat = q >= 2 || use_e1;
         const int M = need_lat ? opts->lattice_m : 0;
         const int nz = q > 1 ? q : 1;                          // lattice coordinates used
@@ -282,6 +283,7 @@ int cfust_em_init(cfust_ctx **out, const double *y, int64_t n, int32_t p, int32_
         for (int k = 0; k < 8; ++k) { s.z[k] = 1; s.shift[k] = 0.5; }
         for (int k = 0; k < nz && M > 0; ++k) { s.z[k] = opts->lattice_z[k]; s.shift[k] = opts->lattice_shift[k]; }
         s.e1_exact = use_e1 ? 1 : 0;
+        s.family = opts->family;
         s.num_sms = prop.multiProcessorCount;
         const int GK1 = g * s.K + 1;
         auto alloc = [&](void **ptr, size_t bytes) { return cudaMalloc(ptr, bytes < 8 ? 8 : bytes) == cudaSuccess; };

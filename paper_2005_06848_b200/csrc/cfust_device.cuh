@@ -109,6 +109,11 @@ __device__ __forceinline__ double dev_t1_logpdf0(double loc, double s2, double m
     return lgc - 0.5 * log(m * CUDART_PI * s2) - 0.5 * (m + 1.0) * log1p(loc * loc / (m * s2));
 }
 
+// log of the univariate normal density phi(0; loc, s2) (skew-normal family, reading F1).
+__device__ __forceinline__ double dev_n1_logpdf0(double loc, double s2) {
+    return -0.5 * loc * loc / s2 - 0.5 * log(2.0 * CUDART_PI * s2);
+}
+
 // Regularized incomplete gamma: series for P (x < a + 1), Legendre CF for Q otherwise.
 __device__ inline double dev_gamma_series_P(double a, double x) {
     double sum = 1.0 / a, term = sum, ap = a;

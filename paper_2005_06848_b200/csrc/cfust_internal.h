@@ -29,6 +29,7 @@ struct DevState {
     double shift[8];
     int num_sms;
     int e1_exact;                   // 1: exact e1 = E[log W | y] (reading R2'); 0: reading A5
+    int family;                     // 0: skew-t (CFUST); 1: skew-normal (CFUSN, nu = inf; q = 0: Gaussian)
 };
 
 // rows of the per-component node table DevState::chi

@@ -195,7 +195,7 @@ __device__ __noinline__ double T_eval(const double *b, const double *S, int lds,
     if constexpr (R == 0) {
         return 1.0;
     } else if constexpr (R == 1) {
-        return dev_t_cdf(b[0] / sqrt(S[0]), m);
+        return isinf(m) ? Phi(b[0] / sqrt(S[0])) : dev_t_cdf(b[0] / sqrt(S[0]), m);   // m = inf: normal family
     } else {
         double binv[R], Cn[R * (R - 1) / 2];
         if (!sov_setup<R>(b, S, lds, binv, Cn)) return CUDART_NAN;
@@ -232,7 +232,10 @@ __device__ __noinline__ double T_eval_w(const double *b, const double *S, int ld
 // MODE 1 computes only log f (T0).  Results go to res[] (identical in all lanes).
 template <int Q, int MODE>
 __device__ void pair_eval(const CompDev &cp, int p, const double *__restrict__ W, int M, const double *__restrict__ chi,
-                          WarpScratch &ws, double *res, int lane, int e1_exact) {
+                          WarpScratch &ws, double *res, int lane, int e1_exact, int family) {
+    // family 1 = skew-normal (CFUSN, nu = inf; reading F1): W = 1, normal SOV (radius nodes = 1),
+    // normal densities and conditionals; every t-specific factor below becomes 1.
+    const bool nrm = family == 1;
     double r[PMAX], v[PMAX];
     double d = 0.0;
 #pragma unroll
@@ -247,7 +250,8 @@ __device__ void pair_eval(const CompDev &cp, int p, const double *__restrict__ W
         }
     }
     const double nu = cp.nu, m0 = cp.m0, rho = nu + d;
-    const double logt = cp.kappa - 0.5 * m0 * log1p(d / nu);
+    const double logt = nrm ? cp.kappa - 0.5 * d : cp.kappa - 0.5 * m0 * log1p(d / nu);
+    const double mT0 = nrm ? CUDART_INF : m0;   // df of T0 (inf: normal)
     double c[Q];
 #pragma unroll
     for (int k = 0; k < Q; ++k) {
@@ -258,7 +262,7 @@ __device__ void pair_eval(const CompDev &cp, int p, const double *__restrict__ W
         c[k] = s;
     }
     // T0 (density, Eq. (2)) and T2 (for e2)
-    const double sq0 = sqrt(m0 / rho);
+    const double sq0 = nrm ? 1.0 : sqrt(m0 / rho);
 #pragma unroll
     for (int k = 0; k < Q; ++k) ws.b[k] = c[k] * sq0;
     double T0, e1x = 0.0;
@@ -268,24 +272,27 @@ __device__ void pair_eval(const CompDev &cp, int p, const double *__restrict__ W
         T0 = (Q == 1) ? T_eval<1, 1>(ws.b, cp.Lam, QMAX, m0, chi, W, M, lane) : T0lat;   // density: exact T_1
         e1x = wsum / T0lat - log(rho);
     } else {
-        T0 = T_eval<Q, Tune<Q>::NP>(ws.b, cp.Lam, QMAX, m0, chi, W, M, lane);
+        T0 = T_eval<Q, Tune<Q>::NP>(ws.b, cp.Lam, QMAX, mT0, chi, W, M, lane);
     }
     if (MODE == 1) {
         res[0] = (T0 > 0.0) ? Q * CUDART_LN2 + logt + log(T0) : -CUDART_INF;
         return;
     }
-    const double sq2 = sqrt((m0 + 2.0) / rho);
+    double T2 = T0;   // normal family: E1 = c P + Lambda h uses P = T0, and e2 = 1
+    if (!nrm) {
+        const double sq2 = sqrt((m0 + 2.0) / rho);
 #pragma unroll
-    for (int k = 0; k < Q; ++k) ws.b[k] = c[k] * sq2;
-    const double T2 = T_eval<Q, Tune<Q>::NP>(ws.b, cp.Lam, QMAX, m0 + 2.0, chi + CHI_M2 * M, W, M, lane);
-    res[1] = cp.psi_half_m0 - log(0.5 * rho) - m0 / rho;      // e1 - e2, reading A5
+        for (int k = 0; k < Q; ++k) ws.b[k] = c[k] * sq2;
+        T2 = T_eval<Q, Tune<Q>::NP>(ws.b, cp.Lam, QMAX, m0 + 2.0, chi + CHI_M2 * M, W, M, lane);
+    }
+    res[1] = nrm ? 0.0 : cp.psi_half_m0 - log(0.5 * rho) - m0 / rho;      // e1 - e2, reading A5
     if (!(T0 > 0.0)) {                                          // reading A16
         res[0] = -CUDART_INF;
         for (int k = 2; k < 3 + Q + Q * Q; ++k) res[k] = 0.0;
         return;
     }
-    // S' = (rho/m0) Lambda
-    const double sc = rho / m0;
+    // S' = (rho/m0) Lambda  (normal: Lambda)
+    const double sc = nrm ? 1.0 : rho / m0;
 #pragma unroll
     for (int k = 0; k < Q; ++k)
 #pragma unroll
@@ -296,9 +303,9 @@ __device__ void pair_eval(const CompDev &cp, int p, const double *__restrict__ W
     constexpr int Q2 = (Q >= 2) ? Q - 2 : 0;
     for (int k = 0; k < Q; ++k) {
         const double skk = Sp[k * QMAX + k];
-        ws.phi[k] = exp(dev_t1_logpdf0(c[k], skk, m0, cp.lgc_m0));
+        ws.phi[k] = exp(nrm ? dev_n1_logpdf0(c[k], skk) : dev_t1_logpdf0(c[k], skk, m0, cp.lgc_m0));
         if constexpr (Q >= 2) {
-            const double fac = (m0 + c[k] * c[k] / skk) / (m0 + 1.0);
+            const double fac = nrm ? 1.0 : (m0 + c[k] * c[k] / skk) / (m0 + 1.0);
             int ia = 0;
             for (int i = 0; i < Q; ++i) {
                 if (i == k) continue;
@@ -313,7 +320,7 @@ __device__ void pair_eval(const CompDev &cp, int p, const double *__restrict__ W
             }
         }
     }
-    const double rat = (m0 + 1.0) / (m0 - 1.0);   // S~' = rat * S~ (df m0 - 1)
+    const double rat = nrm ? 1.0 : (m0 + 1.0) / (m0 - 1.0);   // S~' = rat * S~ (df m0 - 1)
     // T_{q-2} for each pair {k < t}: condition t_{q-1}(c~(k), S~'(k), m0-1) on x_t = 0 (df m0)
     if constexpr (Q >= 3) {
         for (int k = 0; k < Q; ++k)
@@ -321,7 +328,7 @@ __device__ void pair_eval(const CompDev &cp, int p, const double *__restrict__ W
                 const int at = t - 1;                  // position of t among "others of k" (t > k)
                 const double saa = rat * ws.St[k][at * QMAX + at];
                 const double cta = ws.ct[k][at];
-                const double fac2 = (m0 - 1.0 + cta * cta / saa) / m0;
+                const double fac2 = nrm ? 1.0 : (m0 - 1.0 + cta * cta / saa) / m0;
                 int ib = 0;
                 for (int i = 0; i < Q1; ++i) {
                     if (i == at) continue;
@@ -337,7 +344,7 @@ __device__ void pair_eval(const CompDev &cp, int p, const double *__restrict__ W
                     }
                     ++ib;
                 }
-                const double val = T_eval<Q2, Tune<Q>::NP>(ws.bc, ws.Sc, QMAX, m0, chi, W, M, lane);
+                const double val = T_eval<Q2, Tune<Q>::NP>(ws.bc, ws.Sc, QMAX, mT0, chi, W, M, lane);
                 ws.Tkt[k * QMAX + t] = val;
                 ws.Tkt[t * QMAX + k] = val;            // symmetric in {k, t} (A17)
             }
@@ -347,7 +354,8 @@ __device__ void pair_eval(const CompDev &cp, int p, const double *__restrict__ W
 #pragma unroll
     for (int k = 0; k < Q; ++k) {
         double tk = 1.0;
-        if constexpr (Q >= 2) tk = T_eval<Q1, Tune<Q>::NP>(ws.ct[k], ws.St[k], QMAX, m0 + 1.0, chi + CHI_M1 * M, W, M, lane);
+        if constexpr (Q >= 2)
+            tk = T_eval<Q1, Tune<Q>::NP>(ws.ct[k], ws.St[k], QMAX, nrm ? CUDART_INF : m0 + 1.0, chi + CHI_M1 * M, W, M, lane);
         ws.Tk[k] = tk;
         h[k] = ws.phi[k] * tk;
     }
@@ -373,7 +381,7 @@ __device__ void pair_eval(const CompDev &cp, int p, const double *__restrict__ W
                 const int t = (a < k) ? a : a + 1;
                 const double saa = rat * ws.St[k][a * QMAX + a];
                 const double tkt = (Q >= 3) ? ws.Tkt[k * QMAX + t] : 1.0;
-                hk[a] = exp(dev_t1_logpdf0(ws.ct[k][a], saa, m0 - 1.0, cp.lgc_m0m1)) * tkt;
+                hk[a] = exp(nrm ? dev_n1_logpdf0(ws.ct[k][a], saa) : dev_t1_logpdf0(ws.ct[k][a], saa, m0 - 1.0, cp.lgc_m0m1)) * tkt;
             }
             for (int a = 0; a < Q1; ++a) {
                 const int l = (a < k) ? a : a + 1;
@@ -384,10 +392,10 @@ __device__ void pair_eval(const CompDev &cp, int p, const double *__restrict__ W
         }
     }
     // E2 = sym( S'(G + T0 I) + c E1' );  e2, e3, e4 (O8)
-    const double fr = m0 / rho;
+    const double fr = nrm ? 1.0 : m0 / rho;
     const double inv = 1.0 / T0;
     res[0] = Q * CUDART_LN2 + logt + log(T0);
-    res[2] = fr * T2 * inv;
+    res[2] = nrm ? 1.0 : fr * T2 * inv;
     if (e1_exact) res[1] = e1x - res[2];
 #pragma unroll
     for (int a = 0; a < Q; ++a) res[3 + a] = fr * E1[a] * inv;
@@ -447,6 +455,7 @@ struct EArgs {
     int64_t cnt;
     double *__restrict__ pair_out;
     int e1_exact;                   // 1: exact e1 (reading R2'), 0: reading A5
+    int family;                     // 0 skew-t (CFUST), 1 skew-normal (CFUSN; q = 0: Gaussian)
 };
 
 // MODE 0: E-step statistics; 1: log-likelihood only; 2: per-pair dump of idx[0..cnt).
@@ -477,7 +486,7 @@ __global__ void __launch_bounds__(EW * 32, Tune<Q>::MB) estep_cfust_kernel(EArgs
         __syncwarp();
         for (int i = 0; i < g; ++i)
             pair_eval<Q, MODE == 1 ? 1 : 0>(comp[i], p, A.W, M, A.chi + size_t(i) * CHI_ROWS * M, ws, ws.res[i], lane,
-                                            A.e1_exact);
+                                            A.e1_exact, A.family);
         __syncwarp();
         // Eq. (3)-(4): LSE over components, tau
         double lf[GMAX], mx = -CUDART_INF;
@@ -634,8 +643,8 @@ __global__ void __launch_bounds__(TT, 2) estep_t_kernel(EArgs A, int mode) {
                     d += v[a] * v[a];
                 }
                 dd[i] = d;
-                l1[i] = log1p(d * cp.inv_nu);
-                lf[i] = cp.logpi + cp.kappa - 0.5 * cp.m0 * l1[i];
+                l1[i] = (A.family == 1) ? 0.0 : log1p(d * cp.inv_nu);
+                lf[i] = cp.logpi + cp.kappa - ((A.family == 1) ? 0.5 * d : 0.5 * cp.m0 * l1[i]);
                 mx = fmax(mx, lf[i]);
             }
         }
@@ -654,8 +663,8 @@ __global__ void __launch_bounds__(TT, 2) estep_t_kernel(EArgs A, int mode) {
             if (i < g) {
                 const CompDev &cp = comp[i];
                 const double tau = valid ? lf[i] * ise : 0.0;
-                const double e2 = cp.m0 / (cp.nu + dd[i]);
-                const double e1me2 = cp.psi_half_m0 - (cp.log_half_nu + l1[i]) - e2;   // log(rho/2) = log(nu/2) + log1p(d/nu)
+                const double e2 = (A.family == 1) ? 1.0 : cp.m0 / (cp.nu + dd[i]);
+                const double e1me2 = (A.family == 1) ? 0.0 : cp.psi_half_m0 - (cp.log_half_nu + l1[i]) - e2;
                 we[t * WS + i] = tau * e2;
                 wt[t * WS + i] = tau;
                 wl[t * WS + i] = tau * e1me2;
@@ -778,6 +787,7 @@ __global__ void __launch_bounds__(TW * 32, CFUST_T_MB) estep_t_mma_kernel(EArgs 
         reinterpret_cast<double *>(comp)[t] = reinterpret_cast<const double *>(A.comp)[t];
     for (int t = threadIdx.x; t < TW * (GK + 1); t += blockDim.x) red[t] = 0.0;
     __syncthreads();
+    const bool nrm = A.family == 1;
     double s0[G], s1[G], s7[G], s2[G], c0[G], c1[G];
 #pragma unroll
     for (int i = 0; i < G; ++i) s0[i] = s1[i] = s7[i] = s2[i] = c0[i] = c1[i] = 0.0;
@@ -808,8 +818,8 @@ __global__ void __launch_bounds__(TW * 32, CFUST_T_MB) estep_t_mma_kernel(EArgs 
                 }
             }
             dd[i] = d;
-            l1[i] = log1p_pos(d * cp.inv_nu);
-            lf[i] = cp.logpi + cp.kappa - 0.5 * cp.m0 * l1[i];
+            l1[i] = nrm ? 0.0 : log1p_pos(d * cp.inv_nu);
+            lf[i] = cp.logpi + cp.kappa - (nrm ? 0.5 * d : 0.5 * cp.m0 * l1[i]);   // normal: Gaussian component
             mx = fmax(mx, lf[i]);
         }
         double se = 0.0;
@@ -824,8 +834,8 @@ __global__ void __launch_bounds__(TW * 32, CFUST_T_MB) estep_t_mma_kernel(EArgs 
         for (int i = 0; i < G; ++i) {
             const CompDev &cp = comp[i];
             const double tau = valid ? lf[i] * ise : 0.0;
-            const double e2 = div_fast(cp.m0, cp.nu + dd[i]);
-            const double e1me2 = cp.psi_half_m0 - (cp.log_half_nu + l1[i]) - e2;   // log(rho/2) = log(nu/2) + log1p(d/nu)
+            const double e2 = nrm ? 1.0 : div_fast(cp.m0, cp.nu + dd[i]);
+            const double e1me2 = nrm ? 0.0 : cp.psi_half_m0 - (cp.log_half_nu + l1[i]) - e2;   // log(rho/2) = log(nu/2) + log1p(d/nu)
             s0[i] += tau;
             w[i] = tau * e2;
             s1[i] += w[i];
@@ -907,9 +917,15 @@ __global__ void dump_t_kernel(EArgs A) {
                 dd += v[a] * v[a];
             }
             const double rho = cp.nu + dd;
-            lf[i] = cp.logpi + cp.kappa - 0.5 * cp.m0 * log1p(dd / cp.nu);
-            e2[i] = cp.m0 / rho;
-            e1me2[i] = cp.psi_half_m0 - log(0.5 * rho) - e2[i];
+            if (A.family == 1) {   // Gaussian component
+                lf[i] = cp.logpi + cp.kappa - 0.5 * dd;
+                e2[i] = 1.0;
+                e1me2[i] = 0.0;
+            } else {
+                lf[i] = cp.logpi + cp.kappa - 0.5 * cp.m0 * log1p(dd / cp.nu);
+                e2[i] = cp.m0 / rho;
+                e1me2[i] = cp.psi_half_m0 - log(0.5 * rho) - e2[i];
+            }
             mx = fmax(mx, lf[i]);
         }
         double se = 0.0;
@@ -996,7 +1012,8 @@ __device__ int derive_one(const DevState &s, int i, CompDev &cd) {
     const double nu = s.nu[i], m0 = nu + p;
     cd.nu = nu;
     cd.m0 = m0;
-    cd.kappa = lgamma(0.5 * m0) - lgamma(0.5 * nu) - 0.5 * p * log(nu * CUDART_PI) - 0.5 * logdet;
+    cd.kappa = (s.family == 1) ? -0.5 * p * log(2.0 * CUDART_PI) - 0.5 * logdet   // log phi_p normaliser
+                               : lgamma(0.5 * m0) - lgamma(0.5 * nu) - 0.5 * p * log(nu * CUDART_PI) - 0.5 * logdet;
     cd.logpi = log(s.pi[i]);
     cd.psi_half_m0 = dev_digamma(0.5 * m0);
     cd.lgc_m0 = lgamma(0.5 * (m0 + 1.0)) - lgamma(0.5 * m0);
@@ -1076,6 +1093,7 @@ __device__ int mstep_one(const DevState &s, int i) {
         if (!chol_dev(p, Sg, p, Lt, PMAX)) return -4;
     }
     const double cst = S7 / S0;
+    if (s.family == 1) return 0;   // skew-normal / Gaussian: no nu
     double nu;
     if (nu_equation(s.nu_hi, cst) > 0.0) nu = s.nu_hi;
     else if (nu_equation(s.nu_lo, cst) < 0.0) nu = s.nu_lo;
@@ -1127,7 +1145,9 @@ __global__ void chi_kernel(DevState s) {
     for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < total; t += gridDim.x * blockDim.x) {
         const int l = t % M, ik = t / M, i = ik / CHI_ROWS, k = ik % CHI_ROWS;
         const double w = s.W[l];   // coordinate 0 drives the chi radius
-        if (k == CHI_LV) {   // only used (and only computed) with exact e1
+        if (s.family == 1) {   // normal SOV: every radius node is 1
+            s.chi[t] = 1.0;
+        } else if (k == CHI_LV) {   // only used (and only computed) with exact e1
             if (s.e1_exact) s.chi[t] = log(dev_chi2_quantile(w, s.comp[i].m0));
         } else {
             const double m = s.comp[i].m0 + double(k);
@@ -1317,6 +1337,7 @@ int launch_estep(const DevState &s, int mode, const int64_t *idx, int64_t cnt, d
     a.cnt = cnt;
     a.pair_out = pair_out;
     a.e1_exact = s.e1_exact;
+    a.family = s.family;
     *nblocks_out = 0;
     if (s.q == 0) {
         if (mode == 2) {

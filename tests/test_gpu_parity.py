@@ -64,8 +64,9 @@ def compare_pairs(got, ref, q, gaps=None, tol=TOL):
     errs = {}
     errs["logf"] = np.max(np.abs(g_[:, 0] - r_[:, 0]) / np.maximum(1.0, np.abs(r_[:, 0])))
     errs["tau"] = np.max(np.abs(g_[:, 1] - r_[:, 1]) / np.maximum(np.abs(r_[:, 1]), 1e-300))
-    errs["e1me2"] = np.max(np.abs(g_[:, 2] - r_[:, 2]) / np.abs(r_[:, 2]))
-    errs["e2"] = np.max(np.abs(g_[:, 3] - r_[:, 3]) / np.abs(r_[:, 3]))
+    # (skew-normal family: e1 - e2 = 0 and e2 = 1 exactly on both sides)
+    errs["e1me2"] = np.max(np.abs(g_[:, 2] - r_[:, 2]) / np.maximum(np.abs(r_[:, 2]), 1e-300))
+    errs["e2"] = np.max(np.abs(g_[:, 3] - r_[:, 3]) / np.maximum(np.abs(r_[:, 3]), 1e-300))
     if q:
         e3g, e3r = g_[:, 4:4 + q], r_[:, 4:4 + q]
         s3 = np.max(np.abs(e3r), axis=1, keepdims=True)
@@ -304,4 +305,32 @@ def test_e1_exact_fit_parity(cf, orc, cfg_id, n, iters):
     tr_err = np.max(np.abs(res["trace"] - ref["trace"]) / np.abs(ref["trace"]))
     assert tr_err <= TOL, tr_err
     compare_params(res["params"], ref["params"], cfg.q)
+    em.close()
+
+
+# ------------------------------------------------------------------ skew-normal family (NEXT-3, reading F1)
+@pytest.mark.parametrize("cfg_id,n", [(1, 700), (2, 211), (3, 5001), (4, 29), (5, 257)])
+def test_skew_normal_pairs_stats_parity(cf, orc, cfg_id, n):
+    cfg, y, init, lat = _problem(cfg_id, n)
+    em = cf.CfustEM(y, cfg.g, cfg.q, init, lat, family="sn")
+    got = em.pairs(np.arange(n))
+    ref = orc.estep(y, init, cfg.q, _olat(orc, lat), pairs=True, gaps=True, family="sn")
+    compare_pairs(got, ref["pairs"], cfg.q, ref["gaps"])
+    assert not np.any(got[..., 2]) and np.all(got[..., 3] == 1.0)   # e1 - e2 = 0, e2 = 1 (W = 1)
+    ll, st = em.estep(want_stats=True)
+    compare_stats(st, ref["stats"], cfg.p, cfg.q, cfg.g)
+    assert abs(ll - ref["loglik"]) <= TOL * abs(ref["loglik"])
+    em.close()
+
+
+@pytest.mark.parametrize("cfg_id,n,iters", [(1, 1000, 10), (3, 20000, 10), (2, 150, 5)])
+def test_skew_normal_fit_parity(cf, orc, cfg_id, n, iters):
+    cfg, y, init, lat = _problem(cfg_id, n)
+    em = cf.CfustEM(y, cfg.g, cfg.q, init, lat, family="sn")
+    res = em.fit(iters)
+    ref = orc.fit(y, init, cfg.q, _olat(orc, lat), max_iter=iters, family="sn")
+    assert ref["rc"] == 0 and res["n_iter"] == ref["n_iter"] == iters
+    assert np.max(np.abs(res["trace"] - ref["trace"]) / np.abs(ref["trace"])) <= TOL
+    compare_params(res["params"], ref["params"], cfg.q)
+    assert np.array_equal(res["params"]["nu"], np.asarray(init["nu"]))   # nu untouched
     em.close()
