@@ -18,12 +18,15 @@ _SRC = os.path.join(_HERE, "cfust_oracle.c")
 _LIB = os.path.join(_HERE, "libcfust_oracle.so")
 
 OK, EINVAL, ENOTPD, EUNDERFLOW, EEMPTY = 0, -1, -4, -5, -6
-E1_EXACT, FAMILY_SN = 1, 2          # E-step / fit flags (reading R2'; skew-normal family, reading F1)
+E1_EXACT, FAMILY_SN, DIRECT = 1, 2, 4   # E-step / fit flags (reading R2'; family F1; SOV-direct D1)
 FAMILIES = {"st": 0, "sn": FAMILY_SN}   # CFUST (skew-t, default) / CFUSN (skew-normal, nu = inf)
 
 
-def _flags(e1_exact=False, family="st"):
-    return (E1_EXACT if e1_exact else 0) | FAMILIES[family]
+ESTIMATORS = {"analytic": 0, "direct": DIRECT}   # truncated moments: O6-O7 (default) / SOV-direct (D1)
+
+
+def _flags(e1_exact=False, family="st", estimator="analytic"):
+    return (E1_EXACT if e1_exact else 0) | FAMILIES[family] | ESTIMATORS[estimator]
 
 
 def build(force: bool = False) -> str:
@@ -235,7 +238,7 @@ def _params(params: dict, g: int, p: int, q: int):
 
 
 def estep(y, params: dict, q: int, lat: Lattice | None, nthreads=None, pairs=False, gaps=False,
-          e1_exact: bool = False, family: str = "st"):
+          e1_exact: bool = False, family: str = "st", estimator: str = "analytic"):
     """Full E-step.  Returns dict(stats [g*K+1], loglik, pairs [n,g,4+q+q*q] optional)."""
     y = _f64(y)
     n, p = y.shape
@@ -247,7 +250,7 @@ def estep(y, params: dict, q: int, lat: Lattice | None, nthreads=None, pairs=Fal
     po = np.zeros((n, g, 4 + q + q * q)) if pairs else None
     gp = np.full((n, g), np.inf) if gaps else None
     rc = lib().orc_estep(n, p, q, g, _p(y), _p(pi), _p(mu), _p(sg), _p(de), _p(nu),
-                         lat.ptr if lat is not None else None, _nt(nthreads), _flags(e1_exact, family),
+                         lat.ptr if lat is not None else None, _nt(nthreads), _flags(e1_exact, family, estimator),
                          _p(po) if pairs else None, _p(stats), _p(ll), _p(gp) if gaps else None)
     out = {"rc": rc, "stats": stats, "loglik": ll[0]}
     if pairs:
@@ -269,7 +272,8 @@ def mstep(stats, params: dict, p: int, q: int, n_total: float, nu_lo=0.1, nu_hi=
 
 
 def fit(y, params: dict, q: int, lat: Lattice | None, max_iter: int, tol: float = 0.0,
-        nthreads=None, nu_lo=0.1, nu_hi=1000.0, e1_exact: bool = False, family: str = "st"):
+        nthreads=None, nu_lo=0.1, nu_hi=1000.0, e1_exact: bool = False, family: str = "st",
+        estimator: str = "analytic"):
     y = _f64(y)
     n, p = y.shape
     g = len(params["pi"])
@@ -277,7 +281,8 @@ def fit(y, params: dict, q: int, lat: Lattice | None, max_iter: int, tol: float 
     trace = np.zeros(max_iter + 1)
     ni = C.c_int(0); cv = C.c_int(0)
     rc = lib().orc_fit(n, p, q, g, _p(y), _p(pi), _p(mu), _p(sg), _p(de), _p(nu),
-                       lat.ptr if lat is not None else None, _nt(nthreads), _flags(e1_exact, family), int(max_iter),
+                       lat.ptr if lat is not None else None, _nt(nthreads), _flags(e1_exact, family, estimator),
+                       int(max_iter),
                        float(tol),
                        float(nu_lo), float(nu_hi), _p(trace), C.byref(ni), C.byref(cv))
     params_out = {"pi": pi, "mu": mu, "sigma": sg,

@@ -544,6 +544,125 @@ int orc_pair(int p, int q, const double *y, const double *mu, const double *L_om
 }
 
 /* =====================================================================================
+ * SOV-direct truncated-moment estimator (NEXT-3, reading D1; flag ORC_DIRECT).  Instead of the
+ * analytic reduction of O6-O7 to T_{q-1} / T_{q-2} integrals, the moments are estimated on the
+ * SOV points of T0 itself, drawing the last normal coordinate too (lattice coordinate q):
+ *   per point l: s_l = chi node (df m0), w_l = V_l / rho = m0 s_l^2 / rho, b = s_l c sqrt(m0/rho)
+ *   (permuted as T0, ascending c_k / sqrt(Lambda_kk)), e_k and xi_k = Phi^{-1}(u_{l,k+1} e_k) for
+ *   k = 0..q-1, z = C xi (C = chol of the permuted Lambda; Z ~ N(0, Lambda) restricted to Z <= b),
+ *   U = c - z / sqrt(w_l) (the posterior draw of U given W = w_l), f_l = prod_k e_k;
+ *   T0 = (1/M) sum f_l (bit-identical to O4's T0), e2 = sum f w / sum f, e1 = sum f log w / sum f
+ *   (exact, as R2'), e3 = sum f w U / sum f, e4 = sum f w U U' / sum f.
+ * Skew-normal family: w = 1, s_l = 1.  q = 1: the density keeps the exact T_1.
+ * ===================================================================================== */
+int orc_pair_direct(int p, int q, const double *y, const double *mu, const double *L_omega,
+                    const double *A, const double *Lambda, double nu, double kappa, double logdet, int sn,
+                    const orc_lattice *L, const double *chi_m0, const double *lv_m0, double *out,
+                    double *min_key_gap) {
+    double r[PMAX], v[PMAX];
+    for (int a = 0; a < p; ++a) r[a] = y[a] - mu[a];
+    for (int a = 0; a < p; ++a) {
+        double t = r[a];
+        for (int b = 0; b < a; ++b) t -= L_omega[a * p + b] * v[b];
+        v[a] = t / L_omega[a * p + a];
+    }
+    double d = 0.0;
+    for (int a = 0; a < p; ++a) d += v[a] * v[a];
+    const double m0 = nu + p, rho = nu + d;
+    const double logt = sn ? -0.5 * p * log(2.0 * ORC_PI) - 0.5 * logdet - 0.5 * d
+                           : kappa - 0.5 * m0 * log1p(d / nu);
+    const int PW = 3 + q + q * q;
+    if (q == 0) {
+        out[0] = logt;
+        out[1] = sn ? 0.0 : orc_digamma(0.5 * m0) - log(0.5 * rho) - m0 / rho;
+        out[2] = sn ? 1.0 : m0 / rho;
+        return ORC_OK;
+    }
+    double c[QMAX];
+    for (int k = 0; k < q; ++k) {
+        double t = 0.0;
+        for (int a = 0; a < p; ++a) t += A[k * p + a] * r[a];
+        c[k] = t;
+    }
+    const double sq = sn ? 1.0 : sqrt(m0 / rho);
+    double bq[QMAX];
+    for (int k = 0; k < q; ++k) bq[k] = c[k] * sq;
+    int perm[QMAX];
+    double key[QMAX];
+    for (int k = 0; k < q; ++k) { perm[k] = k; key[k] = bq[k] / sqrt(Lambda[k * q + k]); }
+    for (int i = 1; i < q; ++i) {
+        const int pi = perm[i];
+        int j = i - 1;
+        while (j >= 0 && key[perm[j]] > key[pi]) { perm[j + 1] = perm[j]; --j; }
+        perm[j + 1] = pi;
+    }
+    if (min_key_gap)
+        for (int i = 1; i < q; ++i) {
+            const double a = key[perm[i - 1]], bb = key[perm[i]];
+            const double gap = fabs(bb - a) / fmax(1.0, fmax(fabs(a), fabs(bb)));
+            if (gap < *min_key_gap) *min_key_gap = gap;
+        }
+    double Sp[QMAX * QMAX], bp[QMAX], cp[QMAX], C[QMAX * QMAX];
+    for (int i = 0; i < q; ++i) {
+        bp[i] = bq[perm[i]];
+        cp[i] = c[perm[i]];
+        for (int j = 0; j < q; ++j) Sp[i * q + j] = Lambda[perm[i] * q + perm[j]];
+    }
+    if (chol(q, Sp, C) != ORC_OK) return ORC_ENOTPD;
+    double F = 0.0, FW = 0.0, FL = 0.0, F3[QMAX] = {0}, F4[QMAX * QMAX] = {0};
+    const double lrho = log(rho);
+    for (int64_t l = 0; l < L->M; ++l) {
+        const double s = chi_m0[l];
+        double e = orc_norm_cdf(s * bp[0] / C[0]);
+        double f = e;
+        double xi[QMAX];
+        for (int k = 0; k < q; ++k) {
+            if (k > 0) {
+                double acc = s * bp[k];
+                for (int t = 0; t < k; ++t) acc -= C[k * q + t] * xi[t];
+                e = orc_norm_cdf(acc / C[k * q + k]);
+                f *= e;
+            }
+            double u = orc_lattice_w(L, l, k + 1) * e;
+            if (u < ORC_UMIN) u = ORC_UMIN;
+            if (u > ORC_UMAX) u = ORC_UMAX;
+            xi[k] = orc_norm_quantile(u);
+        }
+        const double w = sn ? 1.0 : m0 * s * s / rho;
+        const double sw = sn ? 1.0 : s * sq;                  /* sqrt(w) */
+        double U[QMAX];
+        for (int k = 0; k < q; ++k) {
+            double z = 0.0;
+            for (int t = 0; t <= k; ++t) z += C[k * q + t] * xi[t];
+            U[perm[k]] = cp[k] - z / sw;
+        }
+        F += f;
+        FW += f * w;
+        if (!sn) FL += f * (lv_m0[l] - lrho);
+        for (int a = 0; a < q; ++a) {
+            F3[a] += f * w * U[a];
+            for (int b = a; b < q; ++b) F4[a * q + b] += f * w * U[a] * U[b];
+        }
+    }
+    const double T0lat = F / (double)L->M;
+    const double T0 = (q == 1) ? (sn ? orc_norm_cdf(bq[0] / sqrt(Lambda[0])) : orc_t_cdf(bq[0] / sqrt(Lambda[0]), m0))
+                               : T0lat;
+    if (!(T0 > 0.0) || !(F > 0.0)) {                      /* reading A16 */
+        out[0] = -INFINITY;
+        out[1] = sn ? 0.0 : orc_digamma(0.5 * m0) - log(0.5 * rho) - m0 / rho;
+        for (int k = 2; k < PW; ++k) out[k] = 0.0;
+        return ORC_OK;
+    }
+    out[0] = q * log(2.0) + logt + log(T0);
+    out[2] = FW / F;
+    out[1] = sn ? 0.0 : FL / F - out[2];
+    for (int a = 0; a < q; ++a) out[3 + a] = F3[a] / F;
+    for (int a = 0; a < q; ++a)
+        for (int b = a; b < q; ++b) out[3 + q + a * q + b] = out[3 + q + b * q + a] = F4[a * q + b] / F;
+    return ORC_OK;
+}
+
+/* =====================================================================================
  * Skew-normal family (CFUSN, NEXT-3): the nu -> infinity limit of Eq. (2) (
  * reading F1).  W = 1, so U | y ~ N_q(c, Lambda) restricted to u > 0 and
  *   f = 2^q phi_p(y; mu, Omega) Phi_q(c; 0, Lambda),  e2 = 1,  e3 = E1 / P,  e4 = E2 / P,
@@ -688,9 +807,11 @@ int orc_estep(int64_t n, int p, int q, int g, const double *y,
               double *min_key_gap) {
     if (p < 1 || p > PMAX || q < 0 || q > 6 || g < 1 || n < 0) return ORC_EINVAL;
     const int sn = (flags & ORC_FAMILY_SN) != 0;
-    const int use_e1 = (flags & ORC_E1_EXACT) && q >= 1 && !sn;   /* q = 0: R1 is already exact */
-    const int need_lattice = q >= 2 || use_e1;
-    if (need_lattice && (L == NULL || L->M < 1 || L->s < (q > 1 ? q : 1))) return ORC_EINVAL;
+    const int direct = (flags & ORC_DIRECT) != 0 && q >= 1;
+    const int use_e1 = ((flags & ORC_E1_EXACT) || direct) && q >= 1 && !sn;   /* q = 0: R1 is already exact */
+    const int need_lattice = q >= 2 || use_e1 || direct;
+    const int need_s = direct ? q + 1 : (q > 1 ? q : 1);
+    if (need_lattice && (L == NULL || L->M < 1 || L->s < need_s)) return ORC_EINVAL;
     comp_derived *cd = (comp_derived *)calloc(g, sizeof(comp_derived));
     int rc = ORC_OK;
     for (int i = 0; i < g && rc == ORC_OK; ++i) {
@@ -731,7 +852,10 @@ int orc_estep(int64_t n, int p, int q, int g, const double *y,
             const int64_t j = j0 + jj / g;
             const int i = (int)(jj % g);
             double gap = INFINITY;
-            const int r2 = sn ? orc_pair_sn(p, q, y + (size_t)j * p, mu + (size_t)i * p, cd[i].L, cd[i].A,
+            const int r2 = direct ? orc_pair_direct(p, q, y + (size_t)j * p, mu + (size_t)i * p, cd[i].L, cd[i].A,
+                                                    cd[i].Lam, nu[i], cd[i].kappa, cd[i].logdet, sn, L, cd[i].chi0,
+                                                    cd[i].lv0, buf + (size_t)jj * PW, &gap)
+                         : sn ? orc_pair_sn(p, q, y + (size_t)j * p, mu + (size_t)i * p, cd[i].L, cd[i].A,
                                             cd[i].Lam, cd[i].logdet, L, cd[i].chi0, buf + (size_t)jj * PW, &gap)
                               : orc_pair(p, q, y + (size_t)j * p, mu + (size_t)i * p, cd[i].L, cd[i].A,
                                          cd[i].Lam, nu[i], cd[i].kappa, L, cd[i].chi0, cd[i].chi1,

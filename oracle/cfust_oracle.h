@@ -24,7 +24,7 @@ extern "C" {
 
 enum { ORC_OK = 0, ORC_EINVAL = -1, ORC_ENOTPD = -4, ORC_EUNDERFLOW = -5, ORC_EEMPTY = -6 };
 /* E-step / fit flags: exact e1 (reading R2'); skew-normal family (CFUSN, nu = inf; reading F1) */
-enum { ORC_E1_EXACT = 1, ORC_FAMILY_SN = 2 };
+enum { ORC_E1_EXACT = 1, ORC_FAMILY_SN = 2, ORC_DIRECT = 4 };   /* ORC_DIRECT: SOV-direct moments (D1) */
 
 typedef struct {
     int32_t M;            /* number of lattice points (power of two) */
@@ -72,7 +72,13 @@ int orc_pair_sn(int p, int q, const double *y, const double *mu, const double *L
                 const double *A, const double *Lambda, double logdet, const orc_lattice *L,
                 const double *ones, double *out, double *min_key_gap);
 
-/* ---- E-step over n observations (O9-O10); flags: ORC_E1_EXACT, ORC_FAMILY_SN ----
+/* ---- SOV-direct truncated-moment estimator (reading D1); sn: skew-normal family ---- */
+int orc_pair_direct(int p, int q, const double *y, const double *mu, const double *L_omega,
+                    const double *A, const double *Lambda, double nu, double kappa, double logdet, int sn,
+                    const orc_lattice *L, const double *chi_m0, const double *lv_m0, double *out,
+                    double *min_key_gap);
+
+/* ---- E-step over n observations (O9-O10); flags: ORC_E1_EXACT, ORC_FAMILY_SN, ORC_DIRECT ----
  * pair_out (may be NULL): [n][g][4+q+q*q] = logf, tau, e1me2, e2, e3(q), e4(q*q)
  * stats (may be NULL): [g*K + 1], K = 3+p+p(p+1)/2+q+q(q+1)/2+p*q, last entry = loglik */
 int orc_estep(int64_t n, int p, int q, int g, const double *y,

@@ -174,8 +174,12 @@ def lattice_dims(q: int) -> int:
     return q if q >= 2 else 0
 
 
-def lattice_inputs(cfg: Config, e1_exact: bool = False) -> tuple[int, np.ndarray, np.ndarray]:
-    """(M, z, shift).  e1_exact with q = 1 needs the one chi coordinate (reading R2')."""
+def lattice_inputs(cfg: Config, e1_exact: bool = False, direct: bool = False) -> tuple[int, np.ndarray, np.ndarray]:
+    """(M, z, shift).  e1_exact with q = 1 needs the one chi coordinate (reading R2'); the SOV-direct
+    estimator (reading D1) needs q + 1 coordinates."""
+    if direct and cfg.q >= 1:
+        M = cfg.M or 1024
+        return M, lattice_z(M, cfg.q + 1), lattice_shift(cfg.lattice_seed, cfg.q + 1)
     s = lattice_dims(cfg.q)
     if e1_exact and cfg.q == 1:
         M = cfg.M or 1024

@@ -27,7 +27,7 @@ import os
 import numpy as np
 
 M_LIST = [1 << k for k in range(10, 17)]   # 2^10 .. 2^16 (SURVEY.md §8(b) limits)
-S_MAX = 6                                  # q <= 6 -> chi-normal SOV needs <= q coordinates
+S_MAX = 7                                  # q <= 6: chi-normal SOV needs <= q coordinates; the SOV-direct estimator q+1
 
 
 def omega_table(M: int) -> np.ndarray:
