@@ -291,6 +291,19 @@ def main():
     s_est = sms_[0] / max(1, scnt[0])
     next_rows["skew_normal"] = {"estep_ms": s_est, "pairs_per_s": (j1 - j0) * cfg.g / (s_est * 1e-3)}
     em_s.close()
+    # SOV-direct truncated moments (NEXT-3, reading D1): E-step kernel time on the same workload
+    em_d = cf.CfustEM(yd, cfg.g, cfg.q, init, synth.lattice_inputs(cfg, direct=True), n_total=cfg.n, rank=rank,
+                      world=world, nccl_id=nccl_id_e2e(world, rank, cf, dist) if world > 1 else None, device=local,
+                      timing=True, estimator="direct")
+    em_d.estep()
+    em_d.timing(reset=True)
+    for _ in range(2):
+        em_d.estep()
+    dms, dcnt = em_d.timing(reset=True)
+    d_est = dms[0] / max(1, dcnt[0])
+    next_rows["sov_direct"] = {"estep_ms": d_est, "pairs_per_s": (j1 - j0) * cfg.g / (d_est * 1e-3),
+                               "speedup_vs_default": (phase_ms[0] / max(1, phase_cnt[0])) / d_est}
+    em_d.close()
     # parallel multi-start initialisation (Alg. 1, NEXT-1): m = 8 candidates (k-means + 7 random),
     # Psi^(0) from partition moments, one density pass each, argmax; wall time on the device stream
     em_i = cf.CfustEM(yd, cfg.g, cfg.q, init, (M, z, sh), n_total=cfg.n, rank=rank, world=world,

@@ -17,8 +17,9 @@
  *  - The context owns all device memory, its CUDA stream, events and (world > 1) the NCCL
  *    communicator until cfust_destroy.  No global state; one context per thread at a time.
  *  - Limits: 1 <= p <= 8, 0 <= q <= 6, 1 <= g <= 8; lattice M a power of two in
- *    [1024, 65536] when q >= 2 or (q == 1 and opts.e1_exact); otherwise no lattice is used.
- *    lattice_z / lattice_shift hold max(q, 1) entries.
+ *    [1024, 65536] when q >= 2 or (q == 1 and opts.e1_exact) or opts.estimator == 1; otherwise
+ *    no lattice is used.  lattice_z / lattice_shift hold max(q, 1) entries (q + 1 with
+ *    opts.estimator == 1).
  *  - There is no CPU fallback: without a CUDA device every call fails with CFUST_ECUDA.
  */
 #ifndef CFUST_H
@@ -75,6 +76,13 @@ typedef struct {
                                       nu -> inf limit; reading F1): e2 = 1, nu is
                                       neither used nor updated; with q = 0 a Gaussian mixture
                                       (PAPER.md:147-151).  NEXT-3. */
+    int32_t estimator;             /* truncated moments e3, e4: 0 = analytic reduction to T_{q-1},
+                                      T_{q-2} integrals (DESIGN.md §3 R-E, default); 1 = SOV-direct
+                                      (reading D1, NEXT-3): estimated on T0's own lattice points with
+                                      the last coordinate drawn — 2q Phi/Phi^-1 per point instead of
+                                      2(2q-1)+q(2q-3)+C(q,2)(2q-5); e1 is then exact.  Needs a lattice
+                                      with q+1 coordinates (lattice_z/shift[q+1]) for every q >= 1.
+                                      The density and tau are identical to estimator 0.  */
 } cfust_opts;
 
 typedef struct {

@@ -58,7 +58,7 @@ class CfustEM:
     def __init__(self, y, g: int, q: int, init: dict, lattice=None, *, n_total: int | None = None,
                  rank: int = 0, world: int = 1, nccl_id: bytes | None = None, device: int = -1,
                  timing: bool = False, nu_lo: float = 0.1, nu_hi: float = 1000.0, e1_exact: bool = False,
-                 global_offset: int = 0, family: str = "st"):
+                 global_offset: int = 0, family: str = "st", estimator: str = "analytic"):
         L = lib()
         self._keep = []
         on_dev = hasattr(y, "data_ptr") and getattr(y, "is_cuda", False)
@@ -76,7 +76,7 @@ class CfustEM:
         self.K = k_stats(p, q)
         prm = self._params_struct(init)
         opts = Opts()
-        if lattice is not None and (q >= 2 or (e1_exact and q >= 1)):
+        if lattice is not None and (q >= 2 or ((e1_exact or estimator == "direct") and q >= 1)):
             M, z, sh = lattice
             zz = np.ascontiguousarray(np.asarray(z, dtype=np.uint32))
             ss = _f64(sh)
@@ -97,6 +97,7 @@ class CfustEM:
         opts.e1_exact = 1 if e1_exact else 0
         opts.global_offset = int(global_offset)
         opts.family = {"st": 0, "sn": 1}[family]   # skew-t (CFUST) / skew-normal (CFUSN; q = 0: Gaussian)
+        opts.estimator = {"analytic": 0, "direct": 1}[estimator]   # truncated moments: O6-O7 / SOV-direct (D1)
         ctx = C.c_void_p()
         rc = L.cfust_em_init(C.byref(ctx), yptr, self.n, self.p, self.g, self.q, C.byref(prm), C.byref(opts))
         if rc != 0:

@@ -30,7 +30,8 @@ class Opts(C.Structure):
                 ("lattice_shift", C.POINTER(C.c_double)), ("nu_lo", C.c_double), ("nu_hi", C.c_double),
                 ("y_on_device", C.c_int32), ("device", C.c_int32), ("rank", C.c_int32), ("world", C.c_int32),
                 ("nccl_id", C.c_void_p), ("n_total", C.c_int64), ("timing", C.c_int32),
-                ("e1_exact", C.c_int32), ("global_offset", C.c_int64), ("family", C.c_int32)]
+                ("e1_exact", C.c_int32), ("global_offset", C.c_int64), ("family", C.c_int32),
+                ("estimator", C.c_int32)]
 
 
 class Result(C.Structure):

@@ -238,10 +238,12 @@ int cfust_em_init(cfust_ctx **out, const double *y, int64_t n, int32_t p, int32_
         }
         if (n > 0 && !y) { rc = fail(ctx, CFUST_EINVAL, "y is NULL"); break; }
         if (opts->family < 0 || opts->family > 1) { rc = fail(ctx, CFUST_EINVAL, "family must be 0 (skew-t) or 1 (skew-normal)"); break; }
-        const bool use_e1 = opts->e1_exact != 0 && q >= 1 && opts->family == 0;   // q = 0: A5 exact; no W for skew-normal
-        const bool need_lat = q >= 2 || use_e1;
+        if (opts->estimator < 0 || opts->estimator > 1) { rc = fail(ctx, CFUST_EINVAL, "estimator must be 0 (analytic) or 1 (SOV-direct)"); break; }
+        const bool direct = opts->estimator == 1 && q >= 1;   // SOV-direct truncated moments (reading D1)
+        const bool use_e1 = (opts->e1_exact != 0 || direct) && q >= 1 && opts->family == 0;   // q = 0: A5 exact; no W for skew-normal
+        const bool need_lat = q >= 2 || use_e1 || direct;
         const int M = need_lat ? opts->lattice_m : 0;
-        const int nz = q > 1 ? q : 1;                          // lattice coordinates used
+        const int nz = direct ? q + 1 : (q > 1 ? q : 1);      // lattice coordinates used
         if (need_lat) {
             if (M < 1024 || M > 65536 || (M & (M - 1)) != 0) {
                 rc = fail(ctx, CFUST_EINVAL, "lattice_m must be a power of two in [1024, 65536]");
@@ -284,6 +286,8 @@ int cfust_em_init(cfust_ctx **out, const double *y, int64_t n, int32_t p, int32_
         for (int k = 0; k < nz && M > 0; ++k) { s.z[k] = opts->lattice_z[k]; s.shift[k] = opts->lattice_shift[k]; }
         s.e1_exact = use_e1 ? 1 : 0;
         s.family = opts->family;
+        s.direct = direct ? 1 : 0;
+        s.nw = nz;
         s.num_sms = prop.multiProcessorCount;
         const int GK1 = g * s.K + 1;
         auto alloc = [&](void **ptr, size_t bytes) { return cudaMalloc(ptr, bytes < 8 ? 8 : bytes) == cudaSuccess; };

@@ -34,8 +34,8 @@ struct CompDev {
 
 struct LatticeDev {
     int M;                        // power of two
-    uint32_t z[QMAX];
-    double shift[QMAX];
+    uint32_t z[QMAX + 1];         // q + 1 coordinates for the SOV-direct estimator (reading D1)
+    double shift[QMAX + 1];
 };
 
 // ------------------------------------------------------------------------------------------

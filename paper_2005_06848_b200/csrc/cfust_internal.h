@@ -30,6 +30,8 @@ struct DevState {
     int num_sms;
     int e1_exact;                   // 1: exact e1 = E[log W | y] (reading R2'); 0: reading A5
     int family;                     // 0: skew-t (CFUST); 1: skew-normal (CFUSN, nu = inf; q = 0: Gaussian)
+    int direct;                     // 1: SOV-direct truncated moments (reading D1); 0: analytic (O6-O7)
+    int nw;                         // lattice coordinates tabulated in W (rows)
 };
 
 // rows of the per-component node table DevState::chi

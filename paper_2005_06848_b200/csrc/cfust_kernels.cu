@@ -228,6 +228,162 @@ __device__ __noinline__ double T_eval_w(const double *b, const double *S, int ld
     return warp_sum(acc) / double(M);
 }
 
+// SOV-direct truncated moments (NEXT-3, reading D1): on T0's own SOV points, the last normal
+// coordinate is drawn too (lattice coordinate Q), giving a posterior draw of (W, U) per point:
+//   w = V/rho (1 for the skew-normal family), U = c - C xi / sqrt(w);  with weight f = prod e_k
+// this lane's shares of  F = sum f, FW = sum f w, FL = sum f log w, F3 = sum f w U (permuted
+// order), F4 = sum f w U U' (permuted, upper, packed) are returned warp-reduced in acc[].
+// The first Q factors e_k are computed exactly as in sov_lane_sum, so T0 = F/M is bit-identical.
+template <int Q>
+__device__ __noinline__ bool sov_direct(const double *b, const double *S, int lds, const double *__restrict__ chi,
+                                        const double *__restrict__ lv, const double *__restrict__ W, int M, int lane,
+                                        double sqf, double m0r, double lrho, int sn, int (&perm)[Q], double *acc) {
+    constexpr int NT = Q * (Q + 1) / 2;
+    double key[Q];
+#pragma unroll
+    for (int k = 0; k < Q; ++k) { perm[k] = k; key[k] = b[k] / sqrt(S[k * lds + k]); }
+    for (int i = 1; i < Q; ++i) {
+        const int pi = perm[i];
+        int j = i - 1;
+        while (j >= 0 && key[perm[j]] > key[pi]) { perm[j + 1] = perm[j]; --j; }
+        perm[j + 1] = pi;
+    }
+    double C[Q][Q];
+    for (int i = 0; i < Q; ++i)
+        for (int j = 0; j <= i; ++j) {
+            double s = S[perm[i] * lds + perm[j]];
+            for (int k = 0; k < j; ++k) s -= C[i][k] * C[j][k];
+            if (i == j) {
+                if (!(s > 1e-300)) return false;
+                C[i][i] = sqrt(s);
+            } else {
+                C[i][j] = s / C[j][j];
+            }
+        }
+    double binv[Q], Cn[Q * (Q - 1) / 2 + 1], Cl[NT], cp[Q];
+#pragma unroll
+    for (int k = 0; k < Q; ++k) { binv[k] = b[perm[k]] / C[k][k]; cp[k] = b[perm[k]] / sqf; }
+#pragma unroll
+    for (int k = 1; k < Q; ++k)
+#pragma unroll
+        for (int t = 0; t < k; ++t) Cn[(k * (k - 1)) / 2 + t] = C[k][t] / C[k][k];
+#pragma unroll
+    for (int k = 0; k < Q; ++k)
+#pragma unroll
+        for (int t = 0; t <= k; ++t) Cl[(k * (k + 1)) / 2 + t] = C[k][t];
+    double F = 0.0, FW = 0.0, FL = 0.0, F3[Q], F4[NT];
+#pragma unroll
+    for (int k = 0; k < Q; ++k) F3[k] = 0.0;
+#pragma unroll
+    for (int k = 0; k < NT; ++k) F4[k] = 0.0;
+    for (int l = lane; l < M; l += 32) {
+        const double s = __ldg(chi + l);
+        double e = Phi(s * binv[0]);
+        double f = e;
+        double xi[Q];
+#pragma unroll
+        for (int k = 0; k < Q; ++k) {
+            if (k > 0) {
+                double a = s * binv[k];
+#pragma unroll
+                for (int t = 0; t < k; ++t) a -= Cn[(k * (k - 1)) / 2 + t] * xi[t];
+                e = Phi(a);
+                f *= e;
+            }
+            double u = __ldg(W + (k + 1) * M + l) * e;
+            u = (u < UMIN) ? UMIN : u;
+            u = (u > UMAX) ? UMAX : u;
+            xi[k] = Phiinv(u);
+        }
+        const double w = sn ? 1.0 : m0r * s * s;
+        const double isw = sn ? 1.0 : div_fast(1.0, s * sqf);   // 1 / sqrt(w)
+        const double fw = f * w;
+        F += f;
+        FW += fw;
+        if (!sn) FL = fma(f, __ldg(lv + l) - lrho, FL);
+        double U[Q];
+#pragma unroll
+        for (int k = 0; k < Q; ++k) {
+            double z = 0.0;
+#pragma unroll
+            for (int t = 0; t <= k; ++t) z = fma(Cl[(k * (k + 1)) / 2 + t], xi[t], z);
+            U[k] = cp[k] - z * isw;
+            F3[k] = fma(fw, U[k], F3[k]);
+        }
+#pragma unroll
+        for (int a = 0; a < Q; ++a)
+#pragma unroll
+            for (int bb = a; bb < Q; ++bb) F4[a * Q - a * (a - 1) / 2 + (bb - a)] = fma(fw * U[a], U[bb], F4[a * Q - a * (a - 1) / 2 + (bb - a)]);
+    }
+    acc[0] = warp_sum(F);
+    acc[1] = warp_sum(FW);
+    acc[2] = warp_sum(FL);
+#pragma unroll
+    for (int k = 0; k < Q; ++k) acc[3 + k] = warp_sum(F3[k]);
+#pragma unroll
+    for (int k = 0; k < NT; ++k) acc[3 + Q + k] = warp_sum(F4[k]);
+    return true;
+}
+
+template <int Q>
+__device__ void pair_eval_direct(const CompDev &cp, int p, const double *__restrict__ W, int M,
+                                 const double *__restrict__ chi, WarpScratch &ws, double *res, int lane, int family) {
+    const bool nrm = family == 1;
+    double r[PMAX], v[PMAX];
+    double d = 0.0;
+#pragma unroll
+    for (int a = 0; a < PMAX; ++a) {
+        if (a < p) {
+            r[a] = ws.y[a] - cp.mu[a];
+            double s = r[a];
+#pragma unroll
+            for (int bb = 0; bb < a; ++bb) s -= cp.L[a * PMAX + bb] * v[bb];
+            v[a] = s * cp.Linv[a];
+            d += v[a] * v[a];
+        }
+    }
+    const double nu = cp.nu, m0 = cp.m0, rho = nu + d;
+    const double logt = nrm ? cp.kappa - 0.5 * d : cp.kappa - 0.5 * m0 * log1p(d / nu);
+    const double sqf = nrm ? 1.0 : sqrt(m0 / rho);
+#pragma unroll
+    for (int k = 0; k < Q; ++k) {
+        double s = 0.0;
+#pragma unroll
+        for (int a = 0; a < PMAX; ++a)
+            if (a < p) s += cp.A[k * PMAX + a] * r[a];
+        ws.b[k] = s * sqf;
+    }
+    constexpr int NT = Q * (Q + 1) / 2;
+    double acc[3 + Q + NT];
+    int perm[Q];
+    const bool ok = sov_direct<Q>(ws.b, cp.Lam, QMAX, chi, chi + CHI_LV * M, W, M, lane, sqf, nrm ? 0.0 : m0 / rho,
+                                  log(rho), family, perm, acc);
+    const double F = ok ? acc[0] : 0.0;
+    double T0 = F / double(M);
+    if (Q == 1) T0 = T_eval<1, 1>(ws.b, cp.Lam, QMAX, nrm ? CUDART_INF : m0, chi, W, M, lane);   // exact T_1
+    const double e1me2_a5 = nrm ? 0.0 : cp.psi_half_m0 - log(0.5 * rho) - m0 / rho;
+    if (!(T0 > 0.0) || !(F > 0.0)) {   // reading A16
+        res[0] = -CUDART_INF;
+        res[1] = e1me2_a5;
+        for (int k = 2; k < 3 + Q + Q * Q; ++k) res[k] = 0.0;
+        return;
+    }
+    const double iF = 1.0 / F;
+    res[0] = Q * CUDART_LN2 + logt + log(T0);
+    res[2] = acc[1] * iF;
+    res[1] = nrm ? 0.0 : acc[2] * iF - res[2];
+#pragma unroll
+    for (int k = 0; k < Q; ++k) res[3 + perm[k]] = acc[3 + k] * iF;
+#pragma unroll
+    for (int a = 0; a < Q; ++a)
+#pragma unroll
+        for (int bb = a; bb < Q; ++bb) {
+            const double val = acc[3 + Q + a * Q - a * (a - 1) / 2 + (bb - a)] * iF;
+            res[3 + Q + perm[a] * Q + perm[bb]] = val;
+            res[3 + Q + perm[bb] * Q + perm[a]] = val;
+        }
+}
+
 // Per pair (observation in ws.y, component cp): O2-O8 of DESIGN.md §3.
 // MODE 1 computes only log f (T0).  Results go to res[] (identical in all lanes).
 template <int Q, int MODE>
@@ -456,10 +612,13 @@ struct EArgs {
     double *__restrict__ pair_out;
     int e1_exact;                   // 1: exact e1 (reading R2'), 0: reading A5
     int family;                     // 0 skew-t (CFUST), 1 skew-normal (CFUSN; q = 0: Gaussian)
+    int direct;                     // 1: SOV-direct truncated moments (reading D1)
 };
 
 // MODE 0: E-step statistics; 1: log-likelihood only; 2: per-pair dump of idx[0..cnt).
-template <int Q, int MODE>
+// DIRECT: SOV-direct truncated moments (reading D1) — a separate instantiation, so the analytic
+// kernel's register allocation is not burdened by the direct path.
+template <int Q, int MODE, bool DIRECT = false>
 __global__ void __launch_bounds__(EW * 32, Tune<Q>::MB) estep_cfust_kernel(EArgs A) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -485,8 +644,13 @@ __global__ void __launch_bounds__(EW * 32, Tune<Q>::MB) estep_cfust_kernel(EArgs
         if (lane < p) ws.y[lane] = A.y[j * p + lane];
         __syncwarp();
         for (int i = 0; i < g; ++i)
-            pair_eval<Q, MODE == 1 ? 1 : 0>(comp[i], p, A.W, M, A.chi + size_t(i) * CHI_ROWS * M, ws, ws.res[i], lane,
-                                            A.e1_exact, A.family);
+        {
+            const double *chi_i = A.chi + size_t(i) * CHI_ROWS * M;
+            if constexpr (DIRECT && MODE != 1)
+                pair_eval_direct<Q>(comp[i], p, A.W, M, chi_i, ws, ws.res[i], lane, A.family);
+            else
+                pair_eval<Q, MODE == 1 ? 1 : 0>(comp[i], p, A.W, M, chi_i, ws, ws.res[i], lane, A.e1_exact, A.family);
+        }
         __syncwarp();
         // Eq. (3)-(4): LSE over components, tau
         double lf[GMAX], mx = -CUDART_INF;
@@ -1147,8 +1311,8 @@ __global__ void chi_kernel(DevState s) {
         const double w = s.W[l];   // coordinate 0 drives the chi radius
         if (s.family == 1) {   // normal SOV: every radius node is 1
             s.chi[t] = 1.0;
-        } else if (k == CHI_LV) {   // only used (and only computed) with exact e1
-            if (s.e1_exact) s.chi[t] = log(dev_chi2_quantile(w, s.comp[i].m0));
+        } else if (k == CHI_LV) {   // only used (and only computed) with exact e1 / the direct estimator
+            if (s.e1_exact || s.direct) s.chi[t] = log(dev_chi2_quantile(w, s.comp[i].m0));
         } else {
             const double m = s.comp[i].m0 + double(k);
             s.chi[t] = sqrt(dev_chi2_quantile(w, m) / m);
@@ -1158,7 +1322,7 @@ __global__ void chi_kernel(DevState s) {
 
 // lattice coordinates W[k][l] = |2 frac((l z_k mod M)/M + shift_k) - 1|, once per context
 __global__ void lattice_kernel(DevState s, LatticeDev L) {
-    const int total = (s.q > 1 ? s.q : 1) * s.M;
+    const int total = s.nw * s.M;
     for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < total; t += gridDim.x * blockDim.x)
         s.W[t] = lattice_w(L, t % s.M, t / s.M);
 }
@@ -1201,7 +1365,7 @@ int launch_special(int which, const double *x, double *y, int64_t n, double aux,
 static LatticeDev make_lattice(const DevState &s) {
     LatticeDev L;
     L.M = s.M > 0 ? s.M : 32;
-    for (int k = 0; k < QMAX; ++k) { L.z[k] = s.z[k]; L.shift[k] = s.shift[k]; }
+    for (int k = 0; k <= QMAX; ++k) { L.z[k] = s.z[k]; L.shift[k] = s.shift[k]; }
     return L;
 }
 
@@ -1230,9 +1394,9 @@ static size_t t_smem(const DevState &s) {
     return sizeof(CompDev) * s.g + sizeof(double) * (size_t(TT) * (YS + 3 * WS) + 32 + tasks);
 }
 
-template <int Q, int MODE>
+template <int Q, int MODE, bool DIRECT = false>
 static int launch_cfust_q(const DevState &s, EArgs &a, cudaStream_t st, int *nb) {
-    auto kern = estep_cfust_kernel<Q, MODE>;
+    auto kern = estep_cfust_kernel<Q, MODE, DIRECT>;
     const size_t sm = cfust_smem(s);
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
     if (e != cudaSuccess) return int(e);
@@ -1252,6 +1416,19 @@ static int launch_cfust_q(const DevState &s, EArgs &a, cudaStream_t st, int *nb)
 
 template <int MODE>
 static int launch_cfust_mode(const DevState &s, EArgs &a, cudaStream_t st, int *nb) {
+    if constexpr (MODE != 1) {
+        if (s.direct) {
+            switch (s.q) {
+                case 1: return launch_cfust_q<1, MODE, true>(s, a, st, nb);
+                case 2: return launch_cfust_q<2, MODE, true>(s, a, st, nb);
+                case 3: return launch_cfust_q<3, MODE, true>(s, a, st, nb);
+                case 4: return launch_cfust_q<4, MODE, true>(s, a, st, nb);
+                case 5: return launch_cfust_q<5, MODE, true>(s, a, st, nb);
+                case 6: return launch_cfust_q<6, MODE, true>(s, a, st, nb);
+                default: return int(cudaErrorInvalidValue);
+            }
+        }
+    }
     switch (s.q) {
         case 1: return launch_cfust_q<1, MODE>(s, a, st, nb);
         case 2: return launch_cfust_q<2, MODE>(s, a, st, nb);
@@ -1338,6 +1515,7 @@ int launch_estep(const DevState &s, int mode, const int64_t *idx, int64_t cnt, d
     a.pair_out = pair_out;
     a.e1_exact = s.e1_exact;
     a.family = s.family;
+    a.direct = s.direct;
     *nblocks_out = 0;
     if (s.q == 0) {
         if (mode == 2) {
@@ -1401,7 +1579,7 @@ int launch_chi(const DevState &s, cudaStream_t st) {
 int launch_lattice(const DevState &s, cudaStream_t st) {
     if (s.M <= 0) return 0;
     const LatticeDev L = make_lattice(s);
-    const int total = (s.q > 1 ? s.q : 1) * s.M;
+    const int total = s.nw * s.M;
     lattice_kernel<<<(total + 127) / 128, 128, 0, st>>>(s, L);
     return int(cudaGetLastError());
 }

@@ -334,3 +334,42 @@ def test_skew_normal_fit_parity(cf, orc, cfg_id, n, iters):
     compare_params(res["params"], ref["params"], cfg.q)
     assert np.array_equal(res["params"]["nu"], np.asarray(init["nu"]))   # nu untouched
     em.close()
+
+
+# ------------------------------------------------------------------ SOV-direct estimator (NEXT-3, reading D1)
+def _problem_direct(cfg_id, n, **kw):
+    cfg = synth.with_n(synth.CONFIGS[cfg_id], n)
+    if kw:
+        cfg = synth.with_(cfg, **kw)
+    y, init, _ = synth.make_problem(cfg)
+    return cfg, y, init, synth.lattice_inputs(cfg, direct=True)
+
+
+@pytest.mark.parametrize("cfg_id,n,kw", [(1, 700, {}), (2, 211, {}), (4, 29, {}), (5, 257, {}),
+                                         (1, 301, {"q": 1, "g": 2}), (2, 101, {"family": "sn"})])
+def test_direct_pairs_and_stats_parity(cf, orc, cfg_id, n, kw):
+    fam = kw.pop("family", "st")
+    cfg, y, init, lat = _problem_direct(cfg_id, n, **kw)
+    em = cf.CfustEM(y, cfg.g, cfg.q, init, lat, estimator="direct", family=fam)
+    got = em.pairs(np.arange(n))
+    ref = orc.estep(y, init, cfg.q, _olat(orc, lat), pairs=True, gaps=True, estimator="direct", family=fam)
+    compare_pairs(got, ref["pairs"], cfg.q, ref["gaps"])
+    ll, st = em.estep(want_stats=True)
+    compare_stats(st, ref["stats"], cfg.p, cfg.q, cfg.g)
+    # same density / tau as the analytic estimator
+    an = cf.CfustEM(y, cfg.g, cfg.q, init, lat, family=fam)
+    assert abs(an.estep() - ll) <= 1e-12 * abs(ll)
+    an.close()
+    em.close()
+
+
+@pytest.mark.parametrize("cfg_id,n,iters", [(1, 1000, 10), (5, 200, 5)])
+def test_direct_fit_parity(cf, orc, cfg_id, n, iters):
+    cfg, y, init, lat = _problem_direct(cfg_id, n)
+    em = cf.CfustEM(y, cfg.g, cfg.q, init, lat, estimator="direct")
+    res = em.fit(iters)
+    ref = orc.fit(y, init, cfg.q, _olat(orc, lat), max_iter=iters, estimator="direct")
+    assert ref["rc"] == 0 and res["n_iter"] == ref["n_iter"] == iters
+    assert np.max(np.abs(res["trace"] - ref["trace"]) / np.abs(ref["trace"])) <= TOL
+    compare_params(res["params"], ref["params"], cfg.q)
+    em.close()
