@@ -25,6 +25,9 @@
 
 #define QMAX 8
 #define PMAX 8
+/* Reading A16: a T_q (or Phi_q) value below the smallest normal double is treated as an
+ * underflow, f_ij = 0 — in gradual underflow the ratios E1/T0, E2/T0 lose their precision. */
+#define ORC_TMIN 2.2250738585072014e-308
 static const double ORC_PI = 3.14159265358979323846;
 static const double ORC_UMIN = 1e-300;                 /* reading A15 */
 static const double ORC_UMAX = 0x1.fffffffffffffp-1;   /* largest double < 1, reading A15 */
@@ -437,7 +440,7 @@ int orc_pair(int p, int q, const double *y, const double *mu, const double *L_om
     for (int k = 0; k < q; ++k) bq[k] = c[k] * sqrt((m0 + 2.0) / rho);
     const double T2 = orc_Tr(q, bq, Lambda, m0 + 2.0, L, chi_m2, min_key_gap);
     const int PW = 3 + q + q * q;
-    if (!(T0 > 0.0)) {                       /* reading A16: f_ij = 0 */
+    if (!(T0 >= ORC_TMIN)) {                 /* reading A16: f_ij = 0 (T0 below the normal FP64 range) */
         out[0] = -INFINITY;
         for (int k = 2; k < PW; ++k) out[k] = 0.0;
         return ORC_OK;
@@ -647,7 +650,7 @@ int orc_pair_direct(int p, int q, const double *y, const double *mu, const doubl
     const double T0lat = F / (double)L->M;
     const double T0 = (q == 1) ? (sn ? orc_norm_cdf(bq[0] / sqrt(Lambda[0])) : orc_t_cdf(bq[0] / sqrt(Lambda[0]), m0))
                                : T0lat;
-    if (!(T0 > 0.0) || !(F > 0.0)) {                      /* reading A16 */
+    if (!(T0 >= ORC_TMIN) || !(F > 0.0)) {                /* reading A16 */
         out[0] = -INFINITY;
         out[1] = sn ? 0.0 : orc_digamma(0.5 * m0) - log(0.5 * rho) - m0 / rho;
         for (int k = 2; k < PW; ++k) out[k] = 0.0;
@@ -707,7 +710,7 @@ int orc_pair_sn(int p, int q, const double *y, const double *mu, const double *L
     }
     const double P = phi_r(q, c, Lambda, L, ones, min_key_gap);
     const int PW = 3 + q + q * q;
-    if (!(P > 0.0)) {
+    if (!(P >= ORC_TMIN)) {                  /* reading A16 */
         out[0] = -INFINITY;
         for (int k = 3; k < PW; ++k) out[k] = 0.0;
         return ORC_OK;

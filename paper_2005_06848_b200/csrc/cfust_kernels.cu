@@ -30,6 +30,9 @@ namespace cfust {
 constexpr int EW = CFUST_EW;     // warps per block of the CFUST E-step
 constexpr int MINB = CFUST_MINB; // resident blocks per SM the register budget must allow
 constexpr int RW = 3 + QMAX + QMAX * QMAX;   // per-component result row in scratch
+// Reading A16: T0 below the smallest normal double is an underflow (f_ij = 0): in gradual underflow
+// the ratios E1/T0, E2/T0 have lost their precision (and 1/T0 overflows).
+constexpr double TMIN = 2.2250738585072014e-308;
 
 // Per-warp scratch for the per-pair setup (written redundantly by all lanes with identical
 // values; every lane computes the same setup — SIMT issues it once per warp).
@@ -362,23 +365,23 @@ __device__ void pair_eval_direct(const CompDev &cp, int p, const double *__restr
     double T0 = F / double(M);
     if (Q == 1) T0 = T_eval<1, 1>(ws.b, cp.Lam, QMAX, nrm ? CUDART_INF : m0, chi, W, M, lane);   // exact T_1
     const double e1me2_a5 = nrm ? 0.0 : cp.psi_half_m0 - log(0.5 * rho) - m0 / rho;
-    if (!(T0 > 0.0) || !(F > 0.0)) {   // reading A16
+    if (!(T0 >= TMIN) || !(F > 0.0)) {   // reading A16
         res[0] = -CUDART_INF;
         res[1] = e1me2_a5;
         for (int k = 2; k < 3 + Q + Q * Q; ++k) res[k] = 0.0;
         return;
     }
-    const double iF = 1.0 / F;
+    // ratios by IEEE division (F may be subnormal)
     res[0] = Q * CUDART_LN2 + logt + log(T0);
-    res[2] = acc[1] * iF;
-    res[1] = nrm ? 0.0 : acc[2] * iF - res[2];
+    res[2] = acc[1] / F;
+    res[1] = nrm ? 0.0 : acc[2] / F - res[2];
 #pragma unroll
-    for (int k = 0; k < Q; ++k) res[3 + perm[k]] = acc[3 + k] * iF;
+    for (int k = 0; k < Q; ++k) res[3 + perm[k]] = acc[3 + k] / F;
 #pragma unroll
     for (int a = 0; a < Q; ++a)
 #pragma unroll
         for (int bb = a; bb < Q; ++bb) {
-            const double val = acc[3 + Q + a * Q - a * (a - 1) / 2 + (bb - a)] * iF;
+            const double val = acc[3 + Q + a * Q - a * (a - 1) / 2 + (bb - a)] / F;
             res[3 + Q + perm[a] * Q + perm[bb]] = val;
             res[3 + Q + perm[bb] * Q + perm[a]] = val;
         }
@@ -431,7 +434,7 @@ __device__ void pair_eval(const CompDev &cp, int p, const double *__restrict__ W
         T0 = T_eval<Q, Tune<Q>::NP>(ws.b, cp.Lam, QMAX, mT0, chi, W, M, lane);
     }
     if (MODE == 1) {
-        res[0] = (T0 > 0.0) ? Q * CUDART_LN2 + logt + log(T0) : -CUDART_INF;
+        res[0] = (T0 >= TMIN) ? Q * CUDART_LN2 + logt + log(T0) : -CUDART_INF;
         return;
     }
     double T2 = T0;   // normal family: E1 = c P + Lambda h uses P = T0, and e2 = 1
@@ -442,7 +445,7 @@ __device__ void pair_eval(const CompDev &cp, int p, const double *__restrict__ W
         T2 = T_eval<Q, Tune<Q>::NP>(ws.b, cp.Lam, QMAX, m0 + 2.0, chi + CHI_M2 * M, W, M, lane);
     }
     res[1] = nrm ? 0.0 : cp.psi_half_m0 - log(0.5 * rho) - m0 / rho;      // e1 - e2, reading A5
-    if (!(T0 > 0.0)) {                                          // reading A16
+    if (!(T0 >= TMIN)) {                                        // reading A16
         res[0] = -CUDART_INF;
         for (int k = 2; k < 3 + Q + Q * Q; ++k) res[k] = 0.0;
         return;
@@ -549,12 +552,12 @@ __device__ void pair_eval(const CompDev &cp, int p, const double *__restrict__ W
     }
     // E2 = sym( S'(G + T0 I) + c E1' );  e2, e3, e4 (O8)
     const double fr = nrm ? 1.0 : m0 / rho;
-    const double inv = 1.0 / T0;
+    // ratios by IEEE division (as the oracle): T0 may be subnormal (log f ~ -800), where 1/T0 = inf
     res[0] = Q * CUDART_LN2 + logt + log(T0);
-    res[2] = nrm ? 1.0 : fr * T2 * inv;
+    res[2] = nrm ? 1.0 : fr * T2 / T0;
     if (e1_exact) res[1] = e1x - res[2];
 #pragma unroll
-    for (int a = 0; a < Q; ++a) res[3 + a] = fr * E1[a] * inv;
+    for (int a = 0; a < Q; ++a) res[3 + a] = fr * E1[a] / T0;
     double E2[Q][Q];
 #pragma unroll
     for (int a = 0; a < Q; ++a)
@@ -568,7 +571,7 @@ __device__ void pair_eval(const CompDev &cp, int p, const double *__restrict__ W
 #pragma unroll
     for (int a = 0; a < Q; ++a)
 #pragma unroll
-        for (int bb = 0; bb < Q; ++bb) res[3 + Q + a * Q + bb] = fr * 0.5 * (E2[a][bb] + E2[bb][a]) * inv;
+        for (int bb = 0; bb < Q; ++bb) res[3 + Q + a * Q + bb] = fr * 0.5 * (E2[a][bb] + E2[bb][a]) / T0;
 }
 
 // Stats entry decode: code = type | i << 4 | a << 8 | b << 12

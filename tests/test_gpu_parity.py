@@ -373,3 +373,26 @@ def test_direct_fit_parity(cf, orc, cfg_id, n, iters):
     assert np.max(np.abs(res["trace"] - ref["trace"]) / np.abs(ref["trace"])) <= TOL
     compare_params(res["params"], ref["params"], cfg.q)
     em.close()
+
+
+@pytest.mark.parametrize("family", ["sn", "st"])
+def test_subnormal_density_pairs(cf, orc, family):
+    """Pairs whose T0 is subnormal (< DBL_MIN; log f ~ -800..-870) on the full cfg5 data with the
+    skew-normal family (found by scripts/debug_sn5.py): reading A16 treats them as underflow
+    (f_ij = 0, tau = 0) on both sides — no inf/NaN reaches the statistics."""
+    import torch
+    cfg = synth.CONFIGS[5]
+    y, init, _ = synth.make_problem(cfg)
+    lat = synth.lattice_inputs(cfg)
+    idx = np.array([45535, 142656, 731696, 976575, 1572711, 2592729])
+    em = cf.CfustEM(torch.from_numpy(y).cuda(), cfg.g, cfg.q, init, lat, family=family)
+    got = em.pairs(idx)
+    ref = orc.estep(y[idx], init, cfg.q, _olat(orc, lat), pairs=True, gaps=True, family=family)
+    assert np.all(np.isfinite(got[..., 1:])) and np.all(np.isfinite(ref["pairs"][..., 1:]))
+    assert np.array_equal(np.isfinite(got[..., 0]), np.isfinite(ref["pairs"][..., 0]))
+    if family == "sn":
+        assert np.all(~np.isfinite(got[:, 5, 0])) and np.all(got[:, 5, 1] == 0.0)   # underflow, tau = 0
+    fin = np.isfinite(ref["pairs"][..., 0])
+    if fin.any():
+        compare_pairs(got[fin][:, None], ref["pairs"][fin][:, None], cfg.q)
+    em.close()
