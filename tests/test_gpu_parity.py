@@ -177,7 +177,7 @@ def test_full_size_sampled(cf, orc, cfg_id, nsample):
     ll, st = em.estep(want_stats=True)
     K = synth.k_stats(cfg.p, cfg.q)
     assert abs(sum(st[i * K] for i in range(cfg.g)) - cfg.n) <= 1e-9 * cfg.n
-    assert np.isfinite(ll)
+    assert np.isfinite(ll) and np.all(np.isfinite(st))
     if cfg.q == 0:
         ref = orc.estep(y, init, 0, None)
         compare_stats(st, ref["stats"], cfg.p, cfg.q, cfg.g)
@@ -395,4 +395,26 @@ def test_subnormal_density_pairs(cf, orc, family):
     fin = np.isfinite(ref["pairs"][..., 0])
     if fin.any():
         compare_pairs(got[fin][:, None], ref["pairs"][fin][:, None], cfg.q)
+    em.close()
+
+
+@pytest.mark.parametrize("cfg_id,opt", [(4, {"estimator": "direct"}), (5, {"estimator": "direct"}),
+                                        (5, {"family": "sn"}), (4, {"family": "sn"}), (2, {"e1_exact": True})])
+def test_full_size_options_finite(cf, orc, cfg_id, opt):
+    """Full BASELINE n with each option: every statistic finite, sum_i S0_i = n, one M-step
+    succeeds; sampled pairs vs the oracle."""
+    import torch
+    cfg = synth.CONFIGS[cfg_id]
+    y, init, _ = synth.make_problem(cfg)
+    lat = synth.lattice_inputs(cfg, e1_exact=opt.get("e1_exact", False), direct=opt.get("estimator") == "direct")
+    em = cf.CfustEM(torch.from_numpy(y).cuda(), cfg.g, cfg.q, init, lat, **opt)
+    ll, st = em.estep(want_stats=True)
+    K = synth.k_stats(cfg.p, cfg.q)
+    assert np.isfinite(ll) and np.all(np.isfinite(st))
+    assert abs(sum(st[i * K] for i in range(cfg.g)) - cfg.n) <= 1e-9 * cfg.n
+    idx = np.linspace(0, cfg.n - 1, 6).astype(np.int64)
+    got = em.pairs(idx)
+    ref = orc.estep(y[idx], init, cfg.q, _olat(orc, lat), pairs=True, gaps=True, **opt)
+    compare_pairs(got, ref["pairs"], cfg.q, ref["gaps"])
+    em.mstep()
     em.close()
