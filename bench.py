@@ -264,60 +264,10 @@ def main():
         t_e2e = float(tt.item())
     em_h.close()
 
-    # NEXT rows on the same workload, E-step kernel time only: exact e1 (NEXT-2)
-    next_rows = {}
-    if cfg.q >= 1:
-        em_x = cf.CfustEM(yd, cfg.g, cfg.q, init, synth.lattice_inputs(cfg, e1_exact=True), n_total=cfg.n,
-                          rank=rank, world=world, nccl_id=nccl_id_e2e(world, rank, cf, dist) if world > 1 else None,
-                          device=local, timing=True, e1_exact=True)
-        em_x.estep()
-        em_x.timing(reset=True)
-        for _ in range(2):
-            em_x.estep()
-        xms, xcnt = em_x.timing(reset=True)
-        x_est = xms[0] / max(1, xcnt[0])
-        next_rows["e1_exact"] = {"estep_ms": x_est, "pairs_per_s": (j1 - j0) * cfg.g / (x_est * 1e-3),
-                                 "overhead_vs_default": x_est / (phase_ms[0] / max(1, phase_cnt[0])) - 1.0}
-        em_x.close()
-    # skew-normal family (CFUSN, nu = inf; NEXT-3): E-step kernel time on the same workload
-    em_s = cf.CfustEM(yd, cfg.g, cfg.q, init, (M, z, sh), n_total=cfg.n, rank=rank, world=world,
-                      nccl_id=nccl_id_e2e(world, rank, cf, dist) if world > 1 else None, device=local,
-                      timing=True, family="sn")
-    em_s.estep()
-    em_s.timing(reset=True)
-    for _ in range(2):
-        em_s.estep()
-    sms_, scnt = em_s.timing(reset=True)
-    s_est = sms_[0] / max(1, scnt[0])
-    next_rows["skew_normal"] = {"estep_ms": s_est, "pairs_per_s": (j1 - j0) * cfg.g / (s_est * 1e-3)}
-    em_s.close()
-    # SOV-direct truncated moments (NEXT-3, reading D1): E-step kernel time on the same workload
-    em_d = cf.CfustEM(yd, cfg.g, cfg.q, init, synth.lattice_inputs(cfg, direct=True), n_total=cfg.n, rank=rank,
-                      world=world, nccl_id=nccl_id_e2e(world, rank, cf, dist) if world > 1 else None, device=local,
-                      timing=True, estimator="direct")
-    em_d.estep()
-    em_d.timing(reset=True)
-    for _ in range(2):
-        em_d.estep()
-    dms, dcnt = em_d.timing(reset=True)
-    d_est = dms[0] / max(1, dcnt[0])
-    next_rows["sov_direct"] = {"estep_ms": d_est, "pairs_per_s": (j1 - j0) * cfg.g / (d_est * 1e-3),
-                               "speedup_vs_default": (phase_ms[0] / max(1, phase_cnt[0])) / d_est}
-    em_d.close()
-    # parallel multi-start initialisation (Alg. 1, NEXT-1): m = 8 candidates (k-means + 7 random),
-    # Psi^(0) from partition moments, one density pass each, argmax; wall time on the device stream
-    em_i = cf.CfustEM(yd, cfg.g, cfg.q, init, (M, z, sh), n_total=cfg.n, rank=rank, world=world,
-                      nccl_id=nccl_id_e2e(world, rank, cf, dist) if world > 1 else None, device=local,
-                      global_offset=j0)
-    torch.cuda.synchronize()
-    t0 = time.perf_counter()
-    em_i.init_partitions(8, seed=2005, kmeans_iters=50, want_labels=False)
-    t1 = time.perf_counter()
-    ll0, best = em_i.init_select(8)
-    t2 = time.perf_counter()
-    next_rows["multistart_init"] = {"m": 8, "partitions_ms": (t1 - t0) * 1e3, "select_ms": (t2 - t1) * 1e3,
-                                    "best": best, "loglik0_best": float(ll0[best])}
-    em_i.close()
+    # NEXT rows on the same workload, one GPU only: the driver's multi-GPU runs time
+    # the main EM step; the options' multi-rank paths use the same all-reduce pattern
+    next_rows = bench_options(cf, cfg, yd, init, (M, z, sh), local,
+                              phase_ms[0] / max(1, phase_cnt[0])) if world == 1 else {}
 
     est_ms = phase_ms[0] / max(1, phase_cnt[0])
     pairs_local = (j1 - j0) * cfg.g
@@ -359,6 +309,45 @@ def main():
     em.close()
     if world > 1:
         dist.destroy_process_group()
+
+
+def bench_options(cf, cfg, yd, init, lat, device, default_est_ms):
+    """E-step kernel time of each option on the bench workload (one GPU, device-resident y):
+    exact e1 (NEXT-2), skew-normal family and SOV-direct moments (NEXT-3), and Alg. 1 multi-start
+    initialisation with m = 8 candidates (NEXT-1)."""
+    import torch
+    rows = {}
+    pairs = cfg.n * cfg.g
+
+    def estep_ms(**kw):
+        latk = synth.lattice_inputs(cfg, e1_exact=kw.get("e1_exact", False), direct=kw.get("estimator") == "direct")
+        em = cf.CfustEM(yd, cfg.g, cfg.q, init, latk, device=device, timing=True, **kw)
+        em.estep()
+        em.timing(reset=True)
+        for _ in range(2):
+            em.estep()
+        ms, cnt = em.timing(reset=True)
+        em.close()
+        return ms[0] / max(1, cnt[0])
+
+    if cfg.q >= 1:
+        t = estep_ms(e1_exact=True)
+        rows["e1_exact"] = {"estep_ms": t, "pairs_per_s": pairs / (t * 1e-3), "overhead_vs_default": t / default_est_ms - 1}
+        t = estep_ms(estimator="direct")
+        rows["sov_direct"] = {"estep_ms": t, "pairs_per_s": pairs / (t * 1e-3), "speedup_vs_default": default_est_ms / t}
+    t = estep_ms(family="sn")
+    rows["skew_normal"] = {"estep_ms": t, "pairs_per_s": pairs / (t * 1e-3)}
+    em = cf.CfustEM(yd, cfg.g, cfg.q, init, lat, device=device)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    em.init_partitions(8, seed=2005, kmeans_iters=50, want_labels=False)
+    t1 = time.perf_counter()
+    ll0, best = em.init_select(8)
+    t2 = time.perf_counter()
+    rows["multistart_init"] = {"m": 8, "partitions_ms": (t1 - t0) * 1e3, "select_ms": (t2 - t1) * 1e3,
+                               "best": best, "loglik0_best": float(ll0[best])}
+    em.close()
+    return rows
 
 
 def nccl_id_e2e(world, rank, cf, dist):
