@@ -76,3 +76,12 @@ def test_t_cdf_chi2_digamma(cf, df):
     assert np.max(np.abs(q / st.chi2.ppf(w, df) - 1)) < 1e-12
     d = cf.eval_special("digamma", np.array([0.05, 0.5, 1.0, 2.5, 10.0, 77.0, df]))
     assert np.max(np.abs(d - sp.digamma([0.05, 0.5, 1.0, 2.5, 10.0, 77.0, df]))) < 1e-13
+
+
+def test_trigamma_and_digamma_range(cf):
+    """psi and psi' (the M-step's nu equation and its Newton derivative) vs scipy over the nu range."""
+    x = np.concatenate([np.linspace(0.05, 40, 800), [0.5, 1.0, 16.0, 100.0, 500.0]])
+    tg = cf.eval_special("trigamma", x)
+    assert np.max(np.abs(tg / sp.polygamma(1, x) - 1)) < 5e-15
+    dg = cf.eval_special("digamma", x)
+    assert np.max(np.abs(dg - sp.digamma(x)) / np.maximum(1, np.abs(sp.digamma(x)))) < 2e-15
