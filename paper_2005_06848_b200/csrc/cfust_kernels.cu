@@ -1152,10 +1152,14 @@ __device__ inline void chol_solve_dev(int n, const double *L, int ldl, double *x
 }
 
 // Derived quantities for component i.
-__device__ int derive_one(const DevState &s, int i, CompDev &cd) {
+// Works on thread-local copies (L1-cached local memory) and writes the CompDev once at the end:
+// reading back just-written global memory inside the Cholesky / solve loops went to L2 each time.
+__device__ int derive_one(const DevState &s, int i, CompDev &cd_out) {
     const int p = s.p, q = s.q;
-    const double *Sg = s.sigma + size_t(i) * p * p;
-    const double *D = s.delta + size_t(i) * p * q;
+    double Sg[PMAX * PMAX], D[PMAX * QMAX];
+    for (int t = 0; t < p * p; ++t) Sg[t] = s.sigma[size_t(i) * p * p + t];
+    for (int t = 0; t < p * q; ++t) D[t] = s.delta[size_t(i) * p * q + t];
+    CompDev cd;
     double Om[PMAX * PMAX];
     if (!chol_dev(p, Sg, p, Om, PMAX)) return -4;   // Sigma itself must be PD
     for (int a = 0; a < p; ++a)
@@ -1201,6 +1205,7 @@ __device__ int derive_one(const DevState &s, int i, CompDev &cd) {
     cd.lgc_m0m1 = lgamma(0.5 * m0) - lgamma(0.5 * (m0 - 1.0));
     cd.inv_nu = 1.0 / nu;
     cd.log_half_nu = log(0.5 * nu);
+    cd_out = cd;
     return 0;
 }
 
@@ -1232,7 +1237,9 @@ __device__ int mstep_one(const DevState &s, int i) {
         for (int k = 0; k < q; ++k)
             for (int l = k; l < q; ++l) { S5[k * QMAX + l] = S5p[o]; S5[l * QMAX + k] = S5p[o]; ++o; }
     }
-    double *mu = s.mu + size_t(i) * p, *Sg = s.sigma + size_t(i) * p * p, *D = s.delta + size_t(i) * p * q;
+    // thread-local working copies; Psi is written back once at the end (no global read-after-write)
+    double mu[PMAX], Sg[PMAX * PMAX], D[PMAX * QMAX];
+    for (int t = 0; t < p * q; ++t) D[t] = s.delta[size_t(i) * p * q + t];
     for (int a = 0; a < p; ++a) {
         double v = S2[a];
         for (int k = 0; k < q; ++k) v -= D[a * q + k] * S4[k];
@@ -1273,6 +1280,9 @@ __device__ int mstep_one(const DevState &s, int i) {
         for (int a = 0; a < p; ++a) Sg[a * p + a] += 1e-8 * md;
         if (!chol_dev(p, Sg, p, Lt, PMAX)) return -4;
     }
+    for (int a = 0; a < p; ++a) s.mu[size_t(i) * p + a] = mu[a];
+    for (int t = 0; t < p * p; ++t) s.sigma[size_t(i) * p * p + t] = Sg[t];
+    for (int t = 0; t < p * q; ++t) s.delta[size_t(i) * p * q + t] = D[t];
     const double cst = S7 / S0;
     if (s.family == 1) return 0;   // skew-normal / Gaussian: no nu
     // Root of g(nu) = log(nu/2) - psi(nu/2) + 1 + S7/S0 on [nu_lo, nu_hi] (reading A7; g decreasing,
