@@ -621,8 +621,11 @@ struct EArgs {
 // MODE 0: E-step statistics; 1: log-likelihood only; 2: per-pair dump of idx[0..cnt).
 // DIRECT: SOV-direct truncated moments (reading D1) — a separate instantiation, so the analytic
 // kernel's register allocation is not burdened by the direct path.
+#ifndef CFUST_MBD
+#define CFUST_MBD 2   // resident blocks/SM for the SOV-direct instantiations (profiles/r01_direct_tuning.log)
+#endif
 template <int Q, int MODE, bool DIRECT = false>
-__global__ void __launch_bounds__(EW * 32, Tune<Q>::MB) estep_cfust_kernel(EArgs A) {
+__global__ void __launch_bounds__(EW * 32, (DIRECT && CFUST_MBD > 0) ? CFUST_MBD : Tune<Q>::MB) estep_cfust_kernel(EArgs A) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const int p = A.p, g = A.g, K = A.K, GK = g * K;
