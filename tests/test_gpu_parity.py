@@ -418,3 +418,29 @@ def test_full_size_options_finite(cf, orc, cfg_id, opt):
     compare_pairs(got, ref["pairs"], cfg.q, ref["gaps"])
     em.mstep()
     em.close()
+
+
+def test_empty_shard_and_max_shapes(cf, orc):
+    """n = 0 (an empty rank shard when world > n): zero statistics, l = 0; the largest shape
+    p = 8, q = 6, g = 8 and the largest lattice M = 2^16 against the oracle."""
+    cfg, y, init, lat = _problem(1, 50)
+    em = cf.CfustEM(np.zeros((0, cfg.p)), cfg.g, cfg.q, init, lat, n_total=50)
+    ll, st = em.estep(want_stats=True)
+    assert ll == 0.0 and not np.any(st)
+    em.close()
+    cmax = synth.with_(synth.CONFIGS[4], n=23, p=8, q=6, g=8, M=1024, pi_kind="dirichlet1", data_seed=4242)
+    y, init, _ = synth.make_problem(cmax)
+    latm = synth.lattice_inputs(cmax)
+    em = cf.CfustEM(y, cmax.g, cmax.q, init, latm)
+    got = em.pairs(np.arange(cmax.n))
+    ref = orc.estep(y, init, cmax.q, _olat(orc, latm), pairs=True, gaps=True)
+    compare_pairs(got, ref["pairs"], cmax.q, ref["gaps"])
+    em.close()
+    cbig = synth.with_(synth.CONFIGS[1], n=9, M=65536)
+    y, init, _ = synth.make_problem(cbig)
+    latb = synth.lattice_inputs(cbig)
+    em = cf.CfustEM(y, cbig.g, cbig.q, init, latb)
+    got = em.pairs(np.arange(cbig.n))
+    ref = orc.estep(y, init, cbig.q, _olat(orc, latb), pairs=True, gaps=True)
+    compare_pairs(got, ref["pairs"], cbig.q, ref["gaps"])
+    em.close()
