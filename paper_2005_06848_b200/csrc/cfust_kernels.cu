@@ -935,7 +935,10 @@ __global__ void __launch_bounds__(TT, 2) estep_t_kernel(EArgs A, int mode) {
 #ifndef CFUST_T_MMA
 #define CFUST_T_MMA 1
 #endif
-constexpr int TW = 8;   // warps per block of the q = 0 kernel
+#ifndef CFUST_TW
+#define CFUST_TW 8
+#endif
+constexpr int TW = CFUST_TW;   // warps per block of the q = 0 kernel
 #ifndef CFUST_T_MB
 #define CFUST_T_MB 2        // blocks per SM (G = 5 spills ~300 B but runs 15% faster than 1 block, profiles/r01_cfg3_mma.log)
 #endif
