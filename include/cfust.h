@@ -121,6 +121,13 @@ int cfust_iterate(cfust_ctx *ctx, double *loglik_out);
 /* Density-only pass (T0 only): l = sum_j log f(y_j; Psi) at the current Psi (Eq. (3)). */
 int cfust_loglik(cfust_ctx *ctx, double *out);
 
+/* Clustering output at the current Psi (density pass, as cfust_loglik): labels_out[n] (may be NULL)
+ * receives the MAP component argmax_i tau_ij (ties -> lowest i; the hard partition of SPEC.md:72),
+ * tau_out[n][g] (may be NULL) the responsibilities tau_ij of Eq. (4), loglik_out
+ * (may be NULL) l.  Local observations of this rank; host buffers, caller-owned.  CFUST_EUNDERFLOW
+ * as cfust_estep. */
+int cfust_predict(cfust_ctx *ctx, int32_t *labels_out, double *tau_out, double *loglik_out);
+
 /* Full fit: E-step, then max_iter x [M-step, E-step] with the Aitken stop when tol > 0
  * (Alg. 4, reading A8); out->loglik_trace gets l^(0..n_iter). */
 int cfust_fit(cfust_ctx *ctx, int32_t max_iter, double tol, cfust_result *out);

@@ -179,6 +179,15 @@ class CfustEM:
                                           _dptr(out)), "cfust_get_pairs")
         return out
 
+    def predict(self):
+        """(labels[n], tau[n, g], loglik) at the current Psi: MAP component and responsibilities."""
+        lab = np.zeros(self.n, dtype=np.int32)
+        tau = np.zeros((self.n, self.g))
+        ll = C.c_double(0.0)
+        self._check(lib().cfust_predict(self._ctx, lab.ctypes.data_as(C.POINTER(C.c_int32)), _dptr(tau), C.byref(ll)),
+                    "cfust_predict")
+        return lab, tau, ll.value
+
     def init_partitions(self, m: int, seed: int, kmeans_iters: int = 50, want_labels: bool = True):
         """Alg. 1 step 1 (readings I1, I2): candidate 0 k-means, 1..m-1 random; labels [m, n]."""
         out = np.zeros((m, self.n), dtype=np.int32) if want_labels else None

@@ -43,7 +43,7 @@ class Result(C.Structure):
 EXPORTS = ["cfust_em_init", "cfust_set_data", "cfust_estep", "cfust_mstep", "cfust_iterate", "cfust_loglik",
            "cfust_fit", "cfust_get_params", "cfust_set_params", "cfust_get_pairs", "cfust_get_timing",
            "cfust_stream", "cfust_launch_count", "cfust_nccl_unique_id", "cfust_eval_special", "cfust_k_stats",
-           "cfust_init_partitions", "cfust_init_select",
+           "cfust_init_partitions", "cfust_init_select", "cfust_predict",
            "cfust_last_error", "cfust_destroy"]
 
 _lib = None
@@ -78,6 +78,7 @@ def lib():
         pi32 = C.POINTER(C.c_int32)
         L.cfust_init_partitions.argtypes = [vp, i32, C.c_uint64, i32, pi32]
         L.cfust_init_select.argtypes = [vp, i32, pi32, i32, dp, pi32]
+        L.cfust_predict.argtypes = [vp, pi32, dp, dp]
         L.cfust_last_error.argtypes = [vp]
         L.cfust_last_error.restype = C.c_char_p
         L.cfust_destroy.argtypes = [vp]

@@ -40,6 +40,8 @@ struct cfust_ctx {
     double *d_init = nullptr;      // mind[n] | cent[g p] | ybar[g p] | sums1 | sums2 | argmax scratch
     int *d_iflag = nullptr;        // [GMAX + 1]: empty flags, valid
     double *h_ipin = nullptr;      // pinned staging for Alg. 1 scalars
+    double *d_tau = nullptr;       // cfust_predict outputs
+    int32_t *d_lab = nullptr;
     std::string err;
 };
 
@@ -216,6 +218,8 @@ void cfust_destroy(cfust_ctx *ctx) {
     cudaFree(ctx->d_init);
     cudaFree(ctx->d_iflag);
     cudaFreeHost(ctx->h_ipin);
+    cudaFree(ctx->d_tau);
+    cudaFree(ctx->d_lab);
     cudaFreeHost(ctx->h_pin);
     cudaFreeHost(ctx->h_status);
     for (auto &e : ctx->ev)
@@ -433,6 +437,33 @@ int cfust_loglik(cfust_ctx *ctx, double *out) {
     rc = fetch_status_and_sync(ctx);
     if (rc) return rc;
     *out = ctx->h_pin[0];
+    return CFUST_OK;
+}
+
+int cfust_predict(cfust_ctx *ctx, int32_t *labels_out, double *tau_out, double *loglik_out) {
+    if (!ctx) return CFUST_EINVAL;
+    DevState &s = ctx->s;
+    CU(cudaSetDevice(ctx->device));
+    if (!ctx->d_tau) {
+        CU(cudaMalloc((void **)&ctx->d_tau, sizeof(double) * size_t(s.n > 0 ? s.n : 1) * s.g));
+        CU(cudaMalloc((void **)&ctx->d_lab, sizeof(int32_t) * size_t(s.n > 0 ? s.n : 1)));
+    }
+    int rc = reset_status(ctx);
+    if (rc) return rc;
+    s.tau_out = ctx->d_tau;
+    s.label_out = ctx->d_lab;
+    rc = enqueue_estep(ctx, 1);
+    s.tau_out = nullptr;
+    s.label_out = nullptr;
+    if (rc) return rc;
+    CU(cudaMemcpyAsync(ctx->h_pin, ctx->d_ll, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    if (labels_out && s.n > 0)
+        CU(cudaMemcpyAsync(labels_out, ctx->d_lab, sizeof(int32_t) * s.n, cudaMemcpyDeviceToHost, ctx->stream));
+    if (tau_out && s.n > 0)
+        CU(cudaMemcpyAsync(tau_out, ctx->d_tau, sizeof(double) * s.n * s.g, cudaMemcpyDeviceToHost, ctx->stream));
+    rc = fetch_status_and_sync(ctx);
+    if (rc) return rc;
+    if (loglik_out) *loglik_out = ctx->h_pin[0];
     return CFUST_OK;
 }
 

@@ -616,6 +616,8 @@ struct EArgs {
     int e1_exact;                   // 1: exact e1 (reading R2'), 0: reading A5
     int family;                     // 0 skew-t (CFUST), 1 skew-normal (CFUSN; q = 0: Gaussian)
     int direct;                     // 1: SOV-direct truncated moments (reading D1)
+    double *__restrict__ tau_out;   // MODE 1: tau [n][g] (NULL: log-likelihood only)
+    int32_t *__restrict__ label_out;   // MODE 1: MAP component per observation
 };
 
 // MODE 0: E-step statistics; 1: log-likelihood only; 2: per-pair dump of idx[0..cnt).
@@ -673,7 +675,17 @@ __global__ void __launch_bounds__(EW * 32, (DIRECT && CFUST_MBD > 0) ? CFUST_MBD
             if (i < g) se += exp(lf[i] - mx);
         const double lse = mx + log(se);
         ll += lse;
-        if constexpr (MODE == 1) continue;
+        if constexpr (MODE == 1) {
+            if (A.tau_out && lane == 0) {   // responsibilities and the MAP label (ties -> lowest index)
+                int best = 0;
+                for (int i = 0; i < g; ++i) {
+                    A.tau_out[size_t(j) * g + i] = exp(lf[i] - lse);
+                    if (lf[i] > lf[best]) best = i;
+                }
+                A.label_out[j] = best;
+            }
+            continue;
+        }
         double tau[GMAX];
 #pragma unroll
         for (int i = 0; i < GMAX; ++i) tau[i] = (i < g) ? exp(lf[i] - lse) : 0.0;
@@ -1000,8 +1012,20 @@ __global__ void __launch_bounds__(TW * 32, CFUST_T_MB) estep_t_mma_kernel(EArgs 
         for (int i = 0; i < G; ++i) { lf[i] = exp_neg(lf[i] - mx); se += lf[i]; }   // lf <- exp(lf - max)
         if (valid && mx == -CUDART_INF) atomicOr(A.status, 1);
         if (valid) ll += mx + log_unit(se);
-        if (mode == 1) continue;
         const double ise = div_fast(1.0, se);
+        if (mode == 1) {
+            if (A.tau_out && valid) {   // responsibilities and the MAP label (ties -> lowest index)
+                int best = 0;
+                double bv = lf[0];
+#pragma unroll
+                for (int i = 0; i < G; ++i) {
+                    A.tau_out[size_t(j) * G + i] = lf[i] * ise;
+                    if (lf[i] > bv) { bv = lf[i]; best = i; }
+                }
+                A.label_out[j] = best;
+            }
+            continue;
+        }
         double w[G];
 #pragma unroll
         for (int i = 0; i < G; ++i) {
@@ -1559,6 +1583,8 @@ int launch_estep(const DevState &s, int mode, const int64_t *idx, int64_t cnt, d
     a.e1_exact = s.e1_exact;
     a.family = s.family;
     a.direct = s.direct;
+    a.tau_out = s.tau_out;
+    a.label_out = s.label_out;
     *nblocks_out = 0;
     if (s.q == 0) {
         if (mode == 2) {

@@ -444,3 +444,21 @@ def test_empty_shard_and_max_shapes(cf, orc):
     ref = orc.estep(y, init, cbig.q, _olat(orc, latb), pairs=True, gaps=True)
     compare_pairs(got, ref["pairs"], cbig.q, ref["gaps"])
     em.close()
+
+
+@pytest.mark.parametrize("cfg_id,n,opt", [(2, 301, {}), (3, 4001, {}), (5, 333, {"family": "sn"}), (1, 500, {})])
+def test_predict_labels_and_tau(cf, orc, cfg_id, n, opt):
+    """cfust_predict: tau_ij (Eq. (4)) vs the oracle's, MAP labels = argmax (ties -> lowest index; the
+    hard partition) wherever the oracle's top two tau differ by more than 1e-9."""
+    cfg, y, init, lat = _problem(cfg_id, n)
+    em = cf.CfustEM(y, cfg.g, cfg.q, init, lat, **opt)
+    lab, tau, ll = em.predict()
+    ref = orc.estep(y, init, cfg.q, _olat(orc, lat), pairs=True, **opt)
+    rt = ref["pairs"][:, :, 1]
+    assert np.max(np.abs(tau - rt) / np.maximum(np.abs(rt), 1e-300)) <= TOL
+    assert np.allclose(tau.sum(1), 1.0, atol=1e-12)
+    srt = np.sort(rt, axis=1)
+    clear = srt[:, -1] - srt[:, -2] > 1e-9 if cfg.g > 1 else np.ones(n, bool)
+    assert np.array_equal(lab[clear], rt.argmax(1)[clear])
+    assert abs(ll - ref["loglik"]) <= TOL * abs(ref["loglik"])
+    em.close()
