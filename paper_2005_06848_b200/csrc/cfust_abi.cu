@@ -171,7 +171,7 @@ int enqueue_estep(cfust_ctx *ctx, int mode) {
 int enqueue_mstep(cfust_ctx *ctx) {
     CUI(launch_mstep(ctx->s, ctx->stream));
     CUI(launch_chi(ctx->s, ctx->stream));
-    ctx->launches += (ctx->s.M > 0) ? 2 : 1;
+    ctx->launches += (ctx->s.M > 0) ? 3 : 2;   // M-step, pi + derive, chi nodes
     rec(ctx, 4);
     return CFUST_OK;
 }

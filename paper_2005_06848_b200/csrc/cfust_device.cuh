@@ -67,11 +67,11 @@ __device__ inline double dev_digamma(double x) {
 // trigamma psi'(x), x > 0: recurrence sum 1/(x+k)^2 to x >= 16, then the asymptotic series
 // 1/x + 1/(2x^2) + 1/(6x^3) - 1/(30x^5) + 1/(42x^7) - 1/(30x^9) + 5/(66x^11) (error < 1e-15 there).
 __device__ inline double dev_trigamma(double x) {
-    double acc = 0.0;
-    while (x < 16.0) { acc += 1.0 / (x * x); x += 1.0; }
+    double num = 0.0, den = 1.0;
+    while (x < 16.0) { const double x2 = x * x; num = fma(num, x2, den); den *= x2; x += 1.0; }   // num/den += 1/x^2
     const double r = 1.0 / x, r2 = r * r;
     const double ser = r * (1.0 + r * (0.5 + r * (1.0 / 6 - r2 * (1.0 / 30 - r2 * (1.0 / 42 - r2 * (1.0 / 30 - r2 * (5.0 / 66)))))));
-    return acc + ser;
+    return num / den + ser;
 }
 
 // Continued fraction of the regularized incomplete beta (modified Lentz):

@@ -1240,8 +1240,8 @@ __device__ int derive_one(const DevState &s, int i, CompDev &cd_out) {
 }
 
 __global__ void derive_kernel(DevState s) {
-    const int i = threadIdx.x;
-    if (i < s.g) {
+    const int i = blockIdx.x;
+    if (threadIdx.x == 0 && i < s.g) {
         const int rc = derive_one(s, i, s.comp[i]);
         if (rc != 0) atomicMin(s.status + 1, rc);
     }
@@ -1340,31 +1340,31 @@ __device__ int mstep_one(const DevState &s, int i) {
     return 0;
 }
 
+// M-step, one block per component (thread 0): the components' data-dependent loops (nu iterations,
+// digamma recurrences, lgamma branches) no longer serialise against each other inside one warp.
 __global__ void mstep_kernel(DevState s) {
-    const int i = threadIdx.x;
-    __shared__ int bad;
-    if (i == 0) bad = 0;
-    __syncthreads();
-    if (i < s.g) {
-        const int rc = mstep_one(s, i);
-        if (rc != 0) { atomicMin(s.status + 1, rc); bad = 1; }
+    const int i = blockIdx.x;
+    if (threadIdx.x != 0 || i >= s.g) return;
+    const int rc = mstep_one(s, i);
+    if (rc != 0) atomicMin(s.status + 1, rc);
+}
+
+// pi <- S0 / n_total, floored at 1e-10, renormalised (every block recomputes the total in the same
+// order), then the derived quantities of its component; skipped entirely if any M-step failed.
+__global__ void mstep_derive_kernel(DevState s) {
+    const int i = blockIdx.x;
+    if (threadIdx.x != 0 || i >= s.g) return;
+    if (s.status[1] < 0) return;
+    double tot = 0.0, mine = 0.0;
+    for (int c = 0; c < s.g; ++c) {
+        double v = s.stats[size_t(c) * s.K] / s.n_total;
+        v = (v < 1e-10) ? 1e-10 : v;
+        tot += v;
+        if (c == i) mine = v;
     }
-    __syncthreads();
-    if (i == 0 && !bad) {   // pi <- S0 / n_total, floored at 1e-10, renormalised
-        double tot = 0.0;
-        for (int c = 0; c < s.g; ++c) {
-            double v = s.stats[size_t(c) * s.K] / s.n_total;
-            v = (v < 1e-10) ? 1e-10 : v;
-            s.pi[c] = v;
-            tot += v;
-        }
-        for (int c = 0; c < s.g; ++c) s.pi[c] /= tot;
-    }
-    __syncthreads();
-    if (i < s.g && !bad) {
-        const int rc = derive_one(s, i, s.comp[i]);
-        if (rc != 0) atomicMin(s.status + 1, rc);
-    }
+    s.pi[i] = mine / tot;
+    const int rc = derive_one(s, i, s.comp[i]);
+    if (rc != 0) atomicMin(s.status + 1, rc);
 }
 
 // chi radius nodes: chi[(i*CHI_ROWS + k)*M + l] = sqrt(chi2_{m0+k}^{-1}(w_{l,0}) / (m0+k)), k = 0,1,2;
@@ -1629,12 +1629,13 @@ int launch_reduce_cols(const double *partials, int nblocks, int stride, int ncol
 }
 
 int launch_mstep(const DevState &s, cudaStream_t st) {
-    mstep_kernel<<<1, 32, 0, st>>>(s);
+    mstep_kernel<<<s.g, 32, 0, st>>>(s);
+    mstep_derive_kernel<<<s.g, 32, 0, st>>>(s);
     return int(cudaGetLastError());
 }
 
 int launch_derive(const DevState &s, cudaStream_t st) {
-    derive_kernel<<<1, 32, 0, st>>>(s);
+    derive_kernel<<<s.g, 32, 0, st>>>(s);
     return int(cudaGetLastError());
 }
 
