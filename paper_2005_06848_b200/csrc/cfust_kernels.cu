@@ -552,12 +552,13 @@ __device__ void pair_eval(const CompDev &cp, int p, const double *__restrict__ W
     }
     // E2 = sym( S'(G + T0 I) + c E1' );  e2, e3, e4 (O8)
     const double fr = nrm ? 1.0 : m0 / rho;
-    // ratios by IEEE division (as the oracle): T0 may be subnormal (log f ~ -800), where 1/T0 = inf
+    // T0 >= DBL_MIN here (reading A16 above), so 1/T0 is finite
+    const double inv = 1.0 / T0;
     res[0] = Q * CUDART_LN2 + logt + log(T0);
-    res[2] = nrm ? 1.0 : fr * T2 / T0;
+    res[2] = nrm ? 1.0 : fr * T2 * inv;
     if (e1_exact) res[1] = e1x - res[2];
 #pragma unroll
-    for (int a = 0; a < Q; ++a) res[3 + a] = fr * E1[a] / T0;
+    for (int a = 0; a < Q; ++a) res[3 + a] = fr * E1[a] * inv;
     double E2[Q][Q];
 #pragma unroll
     for (int a = 0; a < Q; ++a)
@@ -571,7 +572,7 @@ __device__ void pair_eval(const CompDev &cp, int p, const double *__restrict__ W
 #pragma unroll
     for (int a = 0; a < Q; ++a)
 #pragma unroll
-        for (int bb = 0; bb < Q; ++bb) res[3 + Q + a * Q + bb] = fr * 0.5 * (E2[a][bb] + E2[bb][a]) / T0;
+        for (int bb = 0; bb < Q; ++bb) res[3 + Q + a * Q + bb] = fr * 0.5 * (E2[a][bb] + E2[bb][a]) * inv;
 }
 
 // Stats entry decode: code = type | i << 4 | a << 8 | b << 12
