@@ -147,6 +147,16 @@ int reset_status(cfust_ctx *ctx) {
     return CFUST_OK;
 }
 
+// world > 1: max-reduce the status word over ranks (status[0] underflow flag, status[1] negative
+// error codes -> reduced as max of -code, status[2] non-finite y) so that all ranks agree.
+int global_status(cfust_ctx *ctx) {
+    if (ctx->world <= 1) return CFUST_OK;
+    NC(ncclAllReduce(ctx->s.status, ctx->s.status, 1, ncclInt32, ncclMax, ctx->comm, ctx->stream));
+    NC(ncclAllReduce(ctx->s.status + 1, ctx->s.status + 1, 1, ncclInt32, ncclMin, ctx->comm, ctx->stream));
+    NC(ncclAllReduce(ctx->s.status + 2, ctx->s.status + 2, 1, ncclInt32, ncclMax, ctx->comm, ctx->stream));
+    return CFUST_OK;
+}
+
 // E-step (mode 0) or loglik (mode 1) up to the global reduction; no host sync.
 int enqueue_estep(cfust_ctx *ctx, int mode) {
     DevState &s = ctx->s;
@@ -163,6 +173,8 @@ int enqueue_estep(cfust_ctx *ctx, int mode) {
         const size_t len = (mode == 1) ? 1 : size_t(s.g) * s.K + 1;
         NC(ncclAllReduce(mode == 1 ? ctx->d_ll : s.stats, mode == 1 ? ctx->d_ll : s.stats, len, ncclDouble, ncclSum,
                          ctx->comm, ctx->stream));
+        int rs = global_status(ctx);   // an underflow on one rank is reported by every rank
+        if (rs) return rs;
     }
     rec(ctx, 3);
     return CFUST_OK;
@@ -333,15 +345,20 @@ int cfust_em_init(cfust_ctx **out, const double *y, int64_t n, int32_t p, int32_
             break;
         }
         ctx->launches += 4;
-        rc = fetch_status_and_sync(ctx);
-        if (rc != CFUST_OK) break;
+        // Multi-rank: the communicator is created BEFORE the validation verdict, and the status word
+        // (non-finite y, derive errors) is max-reduced over ranks, so every rank returns the same
+        // code — a rank failing alone would leave the others blocked in the next collective.
         if (ctx->world > 1) {
             if (!opts->nccl_id) { rc = fail(ctx, CFUST_EINVAL, "world > 1 needs nccl_id"); break; }
             ncclUniqueId id;
             std::memcpy(&id, opts->nccl_id, sizeof(id));
             ncclResult_t r = ncclCommInitRank(&ctx->comm, ctx->world, id, ctx->rank);
             if (r != ncclSuccess) { rc = fail(ctx, CFUST_ENCCL, std::string("ncclCommInitRank: ") + ncclGetErrorString(r)); break; }
+            rc = global_status(ctx);
+            if (rc != CFUST_OK) break;
         }
+        rc = fetch_status_and_sync(ctx);
+        if (rc != CFUST_OK) break;
     } while (0);
     if (rc != CFUST_OK) {
         // keep the message retrievable: return a context only on success; print for the caller
