@@ -1182,76 +1182,46 @@ __device__ inline void chol_solve_dev(int n, const double *L, int ldl, double *x
     }
 }
 
-// Derived quantities for component i.
-// Works on thread-local copies (L1-cached local memory) and writes the CompDev once at the end:
-// reading back just-written global memory inside the Cholesky / solve loops went to L2 each time.
-__device__ int derive_one(const DevState &s, int i, CompDev &cd_out) {
-    const int p = s.p, q = s.q;
-    double Sg[PMAX * PMAX], D[PMAX * QMAX];
-    for (int t = 0; t < p * p; ++t) Sg[t] = s.sigma[size_t(i) * p * p + t];
-    for (int t = 0; t < p * q; ++t) D[t] = s.delta[size_t(i) * p * q + t];
-    CompDev cd;
-    double Om[PMAX * PMAX];
-    if (!chol_dev(p, Sg, p, Om, PMAX)) return -4;   // Sigma itself must be PD
-    for (int a = 0; a < p; ++a)
-        for (int b = 0; b < p; ++b) {
-            double v = Sg[a * p + b];
-            for (int k = 0; k < q; ++k) v += D[a * q + k] * D[b * q + k];
-            Om[a * PMAX + b] = v;
-        }
-    for (int t = 0; t < PMAX * PMAX; ++t) cd.L[t] = 0.0;
-    if (!chol_dev(p, Om, PMAX, cd.L, PMAX)) return -4;
-    double logdet = 0.0;
-    for (int a = 0; a < p; ++a) { cd.Linv[a] = 1.0 / cd.L[a * PMAX + a]; logdet += 2.0 * log(cd.L[a * PMAX + a]); }
-    for (int a = p; a < PMAX; ++a) cd.Linv[a] = 0.0;
-    for (int a = 0; a < p; ++a) cd.mu[a] = s.mu[size_t(i) * p + a];
-    for (int t = 0; t < QMAX * PMAX; ++t) cd.A[t] = 0.0;
-    for (int t = 0; t < QMAX * QMAX; ++t) cd.Lam[t] = 0.0;
-    for (int k = 0; k < q; ++k) {
-        double x[PMAX];
-        for (int a = 0; a < p; ++a) x[a] = D[a * q + k];
-        chol_solve_dev(p, cd.L, PMAX, x);
-        for (int a = 0; a < p; ++a) cd.A[k * PMAX + a] = x[a];
-    }
-    for (int k = 0; k < q; ++k)
-        for (int l = 0; l < q; ++l) {
-            double v = 0.0;
-            for (int a = 0; a < p; ++a) v += D[a * q + k] * cd.A[l * PMAX + a];
-            cd.Lam[k * QMAX + l] = (k == l ? 1.0 : 0.0) - v;
-        }
-    for (int k = 0; k < q; ++k)
-        for (int l = k + 1; l < q; ++l) {
-            const double v = 0.5 * (cd.Lam[k * QMAX + l] + cd.Lam[l * QMAX + k]);
-            cd.Lam[k * QMAX + l] = v;
-            cd.Lam[l * QMAX + k] = v;
-        }
-    const double nu = s.nu[i], m0 = nu + p;
-    cd.nu = nu;
-    cd.m0 = m0;
-    cd.kappa = (s.family == 1) ? -0.5 * p * log(2.0 * CUDART_PI) - 0.5 * logdet   // log phi_p normaliser
-                               : lgamma(0.5 * m0) - lgamma(0.5 * nu) - 0.5 * p * log(nu * CUDART_PI) - 0.5 * logdet;
-    cd.logpi = log(s.pi[i]);
-    cd.psi_half_m0 = dev_digamma(0.5 * m0);
-    cd.lgc_m0 = lgamma(0.5 * (m0 + 1.0)) - lgamma(0.5 * m0);
-    cd.lgc_m0m1 = lgamma(0.5 * m0) - lgamma(0.5 * (m0 - 1.0));
-    cd.inv_nu = 1.0 / nu;
-    cd.log_half_nu = log(0.5 * nu);
-    cd_out = cd;
-    return 0;
-}
 
-__global__ void derive_kernel(DevState s) {
-    const int i = blockIdx.x;
-    if (threadIdx.x == 0 && i < s.g) {
-        const int rc = derive_one(s, i, s.comp[i]);
-        if (rc != 0) atomicMin(s.status + 1, rc);
-    }
-}
 
 __device__ inline double nu_equation(double nu, double c) { return log(0.5 * nu) - dev_digamma(0.5 * nu) + 1.0 + c; }
 
-// M-step for component i (ECM order, reading A6) from the global statistics.
-__device__ int mstep_one(const DevState &s, int i) {
+
+// ------------------------------------------------------------------------------------------
+// M-step (Alg. 3; reading R-M, ECM order) and the derived quantities of each
+// component, one warp per component: every matrix entry is computed by one lane
+// in the plain left-to-right operation order; only independent entries run in parallel.
+
+// Cholesky of the n x n matrix A (row stride lda) into L (stride ldl), column by column: lane 0 the
+// pivot, lanes i > j the column below it.  false (in all lanes) if a pivot is <= 1e-300.
+__device__ bool warp_chol(int n, const double *A, int lda, double *L, int ldl, int lane, int *okflag) {
+    for (int j = 0; j < n; ++j) {
+        if (lane == 0) {
+            double d = A[j * lda + j];
+            for (int k = 0; k < j; ++k) d -= L[j * ldl + k] * L[j * ldl + k];
+            *okflag = (d > 1e-300);
+            L[j * ldl + j] = *okflag ? sqrt(d) : 0.0;
+        }
+        __syncwarp();
+        if (!*okflag) return false;
+        for (int i = j + 1 + lane; i < n; i += 32) {
+            double v = A[i * lda + j];
+            for (int k = 0; k < j; ++k) v -= L[i * ldl + k] * L[j * ldl + k];
+            L[i * ldl + j] = v / L[j * ldl + j];
+        }
+        __syncwarp();
+    }
+    return true;
+}
+
+struct MsWork {
+    double S3[PMAX * PMAX], S5[QMAX * QMAX], mu[PMAX], D[PMAX * QMAX], B[PMAX * QMAX], Sg[PMAX * PMAX];
+    double L5[QMAX * QMAX], Lt[PMAX * PMAX];
+    double md;
+    int ok;
+};
+
+__device__ int mstep_warp(const DevState &s, int i, MsWork &w, int lane) {
     const int p = s.p, q = s.q, K = s.K;
     const double *S = s.stats + size_t(i) * K;
     const double S0 = S[0], S1 = S[1];
@@ -1259,67 +1229,81 @@ __device__ int mstep_one(const DevState &s, int i) {
     const double *S6 = S5p + q * (q + 1) / 2;
     const double S7 = S6[p * q];
     if (!(S0 >= 1e-10)) return -6;
-    double S3[PMAX * PMAX], S5[QMAX * QMAX];
-    {
-        int o = 0;
-        for (int a = 0; a < p; ++a)
-            for (int b = a; b < p; ++b) { S3[a * PMAX + b] = S3p[o]; S3[b * PMAX + a] = S3p[o]; ++o; }
-        o = 0;
-        for (int k = 0; k < q; ++k)
-            for (int l = k; l < q; ++l) { S5[k * QMAX + l] = S5p[o]; S5[l * QMAX + k] = S5p[o]; ++o; }
+    for (int e = lane; e < p * (p + 1) / 2; e += 32) {   // unpack S3 (upper, row-major)
+        int a = 0, r = e;
+        while (r >= p - a) { r -= p - a; ++a; }
+        w.S3[a * PMAX + a + r] = S3p[e];
+        w.S3[(a + r) * PMAX + a] = S3p[e];
     }
-    // thread-local working copies; Psi is written back once at the end (no global read-after-write)
-    double mu[PMAX], Sg[PMAX * PMAX], D[PMAX * QMAX];
-    for (int t = 0; t < p * q; ++t) D[t] = s.delta[size_t(i) * p * q + t];
-    for (int a = 0; a < p; ++a) {
+    for (int e = lane; e < q * (q + 1) / 2; e += 32) {
+        int k = 0, r = e;
+        while (r >= q - k) { r -= q - k; ++k; }
+        w.S5[k * QMAX + k + r] = S5p[e];
+        w.S5[(k + r) * QMAX + k] = S5p[e];
+    }
+    for (int t = lane; t < p * q; t += 32) w.D[t] = s.delta[size_t(i) * p * q + t];
+    __syncwarp();
+    for (int a = lane; a < p; a += 32) {
         double v = S2[a];
-        for (int k = 0; k < q; ++k) v -= D[a * q + k] * S4[k];
-        mu[a] = v / S1;
+        for (int k = 0; k < q; ++k) v -= w.D[a * q + k] * S4[k];
+        w.mu[a] = v / S1;
     }
-    double B[PMAX * QMAX];
-    for (int a = 0; a < p; ++a)
-        for (int k = 0; k < q; ++k) B[a * QMAX + k] = S6[a * q + k] - mu[a] * S4[k];
+    __syncwarp();
+    for (int t = lane; t < p * q; t += 32) {
+        const int a = t / q, k = t % q;
+        w.B[a * QMAX + k] = S6[a * q + k] - w.mu[a] * S4[k];
+    }
+    __syncwarp();
     if (q > 0) {
-        double L5[QMAX * QMAX];
-        if (!chol_dev(q, S5, QMAX, L5, QMAX)) return -4;
-        for (int a = 0; a < p; ++a) {
+        if (!warp_chol(q, w.S5, QMAX, w.L5, QMAX, lane, &w.ok)) return -4;
+        for (int a = lane; a < p; a += 32) {   // row a of B S5^{-1}
             double x[QMAX];
-            for (int k = 0; k < q; ++k) x[k] = B[a * QMAX + k];
-            chol_solve_dev(q, L5, QMAX, x);
-            for (int k = 0; k < q; ++k) D[a * q + k] = x[k];
+            for (int k = 0; k < q; ++k) x[k] = w.B[a * QMAX + k];
+            chol_solve_dev(q, w.L5, QMAX, x);
+            for (int k = 0; k < q; ++k) w.D[a * q + k] = x[k];
         }
+        __syncwarp();
     }
-    for (int a = 0; a < p; ++a)
-        for (int b = 0; b < p; ++b) {
-            double v = S3[a * PMAX + b] - S2[a] * mu[b] - mu[a] * S2[b] + S1 * mu[a] * mu[b];
-            for (int k = 0; k < q; ++k) v -= B[a * QMAX + k] * D[b * q + k] + D[a * q + k] * B[b * QMAX + k];
-            for (int k = 0; k < q; ++k)
-                for (int l = 0; l < q; ++l) v += D[a * q + k] * S5[k * QMAX + l] * D[b * q + l];
-            Sg[a * p + b] = v / S0;
-        }
-    for (int a = 0; a < p; ++a)
-        for (int b = a + 1; b < p; ++b) {
-            const double v = 0.5 * (Sg[a * p + b] + Sg[b * p + a]);
-            Sg[a * p + b] = v;
-            Sg[b * p + a] = v;
-        }
-    double Lt[PMAX * PMAX];
-    if (!chol_dev(p, Sg, p, Lt, PMAX)) {   // ridge repair
-        double md = 0.0;
-        for (int a = 0; a < p; ++a) md += Sg[a * p + a];
-        md /= p;
-        for (int a = 0; a < p; ++a) Sg[a * p + a] += 1e-8 * md;
-        if (!chol_dev(p, Sg, p, Lt, PMAX)) return -4;
+    for (int t = lane; t < p * p; t += 32) {
+        const int a = t / p, b = t % p;
+        double v = w.S3[a * PMAX + b] - S2[a] * w.mu[b] - w.mu[a] * S2[b] + S1 * w.mu[a] * w.mu[b];
+        for (int k = 0; k < q; ++k) v -= w.B[a * QMAX + k] * w.D[b * q + k] + w.D[a * q + k] * w.B[b * QMAX + k];
+        for (int k = 0; k < q; ++k)
+            for (int l = 0; l < q; ++l) v += w.D[a * q + k] * w.S5[k * QMAX + l] * w.D[b * q + l];
+        w.Sg[a * p + b] = v / S0;
     }
-    for (int a = 0; a < p; ++a) s.mu[size_t(i) * p + a] = mu[a];
-    for (int t = 0; t < p * p; ++t) s.sigma[size_t(i) * p * p + t] = Sg[t];
-    for (int t = 0; t < p * q; ++t) s.delta[size_t(i) * p * q + t] = D[t];
+    __syncwarp();
+    double sym[2] = {0.0, 0.0};
+    for (int t = lane, c = 0; t < p * p; t += 32, ++c) {   // symmetrise (reads before writes)
+        const int a = t / p, b = t % p;
+        sym[c] = 0.5 * (w.Sg[a * p + b] + w.Sg[b * p + a]);
+    }
+    __syncwarp();
+    for (int t = lane, c = 0; t < p * p; t += 32, ++c) {
+        const int a = t / p, b = t % p;
+        if (a != b) w.Sg[a * p + b] = sym[c];
+    }
+    __syncwarp();
+    if (!warp_chol(p, w.Sg, p, w.Lt, PMAX, lane, &w.ok)) {   // ridge repair
+        if (lane == 0) {
+            double md = 0.0;
+            for (int a = 0; a < p; ++a) md += w.Sg[a * p + a];
+            w.md = md / p;
+        }
+        __syncwarp();
+        for (int a = lane; a < p; a += 32) w.Sg[a * p + a] += 1e-8 * w.md;
+        __syncwarp();
+        if (!warp_chol(p, w.Sg, p, w.Lt, PMAX, lane, &w.ok)) return -4;
+    }
+    for (int a = lane; a < p; a += 32) s.mu[size_t(i) * p + a] = w.mu[a];
+    for (int t = lane; t < p * p; t += 32) s.sigma[size_t(i) * p * p + t] = w.Sg[t];
+    for (int t = lane; t < p * q; t += 32) s.delta[size_t(i) * p * q + t] = w.D[t];
+    if (s.family == 1 || lane != 0) return 0;   // skew-normal / Gaussian: no nu
     const double cst = S7 / S0;
-    if (s.family == 1) return 0;   // skew-normal / Gaussian: no nu
-    // Root of g(nu) = log(nu/2) - psi(nu/2) + 1 + S7/S0 on [nu_lo, nu_hi] (reading A7; g decreasing,
-    // clamped when there is no sign change): safeguarded Newton from the previous nu, the bracket
-    // kept and bisection taken whenever a step leaves it, to |dnu| <= 1e-13 nu (the oracle bisects to
-    // 1e-12: both land within that tolerance of the root).  ~5 iterations instead of ~50 bisections.
+    // nu: root of g(nu) = log(nu/2) - psi(nu/2) + 1 + S7/S0 on [nu_lo, nu_hi] (reading A7; g decreasing,
+    // clamped when there is no sign change): safeguarded Newton from the previous nu, the bracket kept and
+    // bisection taken whenever a step leaves it, to |dnu| <= 1e-13 nu (the oracle bisects to 1e-12: both
+    // land within that tolerance of the root).
     double nu;
     if (nu_equation(s.nu_hi, cst) > 0.0) nu = s.nu_hi;
     else if (nu_equation(s.nu_lo, cst) < 0.0) nu = s.nu_lo;
@@ -1329,7 +1313,7 @@ __device__ int mstep_one(const DevState &s, int i) {
         for (int it = 0; it < 200; ++it) {
             const double gv = nu_equation(nu, cst);
             if (gv > 0.0) lo = nu; else hi = nu;
-            const double dg = 1.0 / nu - 0.5 * dev_trigamma(0.5 * nu);   // < 0
+            const double dg = 1.0 / nu - 0.5 * dev_trigamma(0.5 * nu);
             double nn = nu - gv / dg;
             if (!(nn > lo && nn < hi)) nn = 0.5 * (lo + hi);
             const bool done = fabs(nn - nu) <= 1e-13 * nu || hi - lo <= 1e-13 * nu;
@@ -1341,31 +1325,124 @@ __device__ int mstep_one(const DevState &s, int i) {
     return 0;
 }
 
-// M-step, one block per component (thread 0): the components' data-dependent loops (nu iterations,
-// digamma recurrences, lgamma branches) no longer serialise against each other inside one warp.
-__global__ void mstep_kernel(DevState s) {
-    const int i = blockIdx.x;
-    if (threadIdx.x != 0 || i >= s.g) return;
-    const int rc = mstep_one(s, i);
-    if (rc != 0) atomicMin(s.status + 1, rc);
+struct DvWork {
+    double Sg[PMAX * PMAX], D[PMAX * QMAX], Om[PMAX * PMAX], Lc[PMAX * PMAX];
+    CompDev cd;
+    double lg[5];
+    int ok;
+};
+
+__device__ int derive_warp(const DevState &s, int i, DvWork &w, CompDev &cd_out, int lane) {
+    const int p = s.p, q = s.q;
+    CompDev &cd = w.cd;
+    for (int t = lane; t < p * p; t += 32) w.Sg[t] = s.sigma[size_t(i) * p * p + t];
+    for (int t = lane; t < p * q; t += 32) w.D[t] = s.delta[size_t(i) * p * q + t];
+    for (int t = lane; t < PMAX * PMAX; t += 32) { cd.L[t] = 0.0; w.Om[t] = 0.0; }
+    for (int t = lane; t < QMAX * PMAX; t += 32) cd.A[t] = 0.0;
+    for (int t = lane; t < QMAX * QMAX; t += 32) cd.Lam[t] = 0.0;
+    __syncwarp();
+    if (!warp_chol(p, w.Sg, p, w.Lc, PMAX, lane, &w.ok)) return -4;   // Sigma itself must be PD
+    for (int t = lane; t < p * p; t += 32) {
+        const int a = t / p, b = t % p;
+        double v = w.Sg[a * p + b];
+        for (int k = 0; k < q; ++k) v += w.D[a * q + k] * w.D[b * q + k];
+        w.Om[a * PMAX + b] = v;
+    }
+    __syncwarp();
+    if (!warp_chol(p, w.Om, PMAX, cd.L, PMAX, lane, &w.ok)) return -4;
+    for (int a = lane; a < PMAX; a += 32) cd.Linv[a] = (a < p) ? 1.0 / cd.L[a * PMAX + a] : 0.0;
+    for (int a = lane; a < p; a += 32) cd.mu[a] = s.mu[size_t(i) * p + a];
+    for (int k = lane; k < q; k += 32) {   // A = Delta' Omega^{-1}: one column of Omega^{-1} Delta per lane
+        double x[PMAX];
+        for (int a = 0; a < p; ++a) x[a] = w.D[a * q + k];
+        chol_solve_dev(p, cd.L, PMAX, x);
+        for (int a = 0; a < p; ++a) cd.A[k * PMAX + a] = x[a];
+    }
+    const double nu = s.nu[i], m0 = nu + p;
+    if (lane < 5) {   // the transcendental constants in parallel
+        double v = 0.0;
+        if (lane == 0) v = lgamma(0.5 * m0) - lgamma(0.5 * nu);
+        else if (lane == 1) v = lgamma(0.5 * (m0 + 1.0)) - lgamma(0.5 * m0);
+        else if (lane == 2) v = lgamma(0.5 * m0) - lgamma(0.5 * (m0 - 1.0));
+        else if (lane == 3) v = dev_digamma(0.5 * m0);
+        else
+            for (int a = 0; a < p; ++a) v += 2.0 * log(cd.L[a * PMAX + a]);
+        w.lg[lane] = v;
+    }
+    __syncwarp();
+    for (int t = lane; t < q * q; t += 32) {
+        const int k = t / q, l = t % q;
+        double v = 0.0;
+        for (int a = 0; a < p; ++a) v += w.D[a * q + k] * cd.A[l * PMAX + a];
+        cd.Lam[k * QMAX + l] = (k == l ? 1.0 : 0.0) - v;
+    }
+    __syncwarp();
+    double sym[2] = {0.0, 0.0};
+    for (int t = lane, c = 0; t < q * q; t += 32, ++c) {
+        const int k = t / q, l = t % q;
+        sym[c] = 0.5 * (cd.Lam[k * QMAX + l] + cd.Lam[l * QMAX + k]);
+    }
+    __syncwarp();
+    for (int t = lane, c = 0; t < q * q; t += 32, ++c) {
+        const int k = t / q, l = t % q;
+        if (k != l) cd.Lam[k * QMAX + l] = sym[c];
+    }
+    if (lane == 0) {
+        const double logdet = w.lg[4];
+        cd.nu = nu;
+        cd.m0 = m0;
+        cd.kappa = (s.family == 1) ? -0.5 * p * log(2.0 * CUDART_PI) - 0.5 * logdet   // log phi_p normaliser
+                                   : w.lg[0] - 0.5 * p * log(nu * CUDART_PI) - 0.5 * logdet;
+        cd.logpi = log(s.pi[i]);
+        cd.psi_half_m0 = w.lg[3];
+        cd.lgc_m0 = w.lg[1];
+        cd.lgc_m0m1 = w.lg[2];
+        cd.inv_nu = 1.0 / nu;
+        cd.log_half_nu = log(0.5 * nu);
+    }
+    __syncwarp();
+    double *dst = reinterpret_cast<double *>(&cd_out);
+    const double *src = reinterpret_cast<const double *>(&cd);
+    for (int t = lane; t < int(sizeof(CompDev) / sizeof(double)); t += 32) dst[t] = src[t];
+    return 0;
+}
+
+// M-step, one warp (block) per component; pi + derive in a second kernel after all components.
+__global__ void __launch_bounds__(32) mstep_kernel(DevState s) {
+    __shared__ MsWork w;
+    const int i = blockIdx.x, lane = threadIdx.x;
+    if (i >= s.g) return;
+    const int rc = mstep_warp(s, i, w, lane);
+    if (rc != 0 && lane == 0) atomicMin(s.status + 1, rc);
 }
 
 // pi <- S0 / n_total, floored at 1e-10, renormalised (every block recomputes the total in the same
 // order), then the derived quantities of its component; skipped entirely if any M-step failed.
-__global__ void mstep_derive_kernel(DevState s) {
-    const int i = blockIdx.x;
-    if (threadIdx.x != 0 || i >= s.g) return;
-    if (s.status[1] < 0) return;
-    double tot = 0.0, mine = 0.0;
-    for (int c = 0; c < s.g; ++c) {
-        double v = s.stats[size_t(c) * s.K] / s.n_total;
-        v = (v < 1e-10) ? 1e-10 : v;
-        tot += v;
-        if (c == i) mine = v;
+__global__ void __launch_bounds__(32) mstep_derive_kernel(DevState s) {
+    __shared__ DvWork w;
+    const int i = blockIdx.x, lane = threadIdx.x;
+    if (i >= s.g || s.status[1] < 0) return;
+    if (lane == 0) {
+        double tot = 0.0, mine = 0.0;
+        for (int c = 0; c < s.g; ++c) {
+            double v = s.stats[size_t(c) * s.K] / s.n_total;
+            v = (v < 1e-10) ? 1e-10 : v;
+            tot += v;
+            if (c == i) mine = v;
+        }
+        s.pi[i] = mine / tot;
     }
-    s.pi[i] = mine / tot;
-    const int rc = derive_one(s, i, s.comp[i]);
-    if (rc != 0) atomicMin(s.status + 1, rc);
+    __syncwarp();
+    const int rc = derive_warp(s, i, w, s.comp[i], lane);
+    if (rc != 0 && lane == 0) atomicMin(s.status + 1, rc);
+}
+
+__global__ void __launch_bounds__(32) derive_kernel(DevState s) {
+    __shared__ DvWork w;
+    const int i = blockIdx.x, lane = threadIdx.x;
+    if (i >= s.g) return;
+    const int rc = derive_warp(s, i, w, s.comp[i], lane);
+    if (rc != 0 && lane == 0) atomicMin(s.status + 1, rc);
 }
 
 // chi radius nodes: chi[(i*CHI_ROWS + k)*M + l] = sqrt(chi2_{m0+k}^{-1}(w_{l,0}) / (m0+k)), k = 0,1,2;
