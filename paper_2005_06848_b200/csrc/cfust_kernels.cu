@@ -1,19 +1,24 @@
 // cfust_kernels.cu — FP64 CUDA kernels of the FM-CFUST EM hot path for sm_100a.
 //
-//   estep_cfust_kernel<Q,MODE>  q >= 1: one warp per observation j, looping over the g
+//   estep_cfust_kernel<Q,MODE,DIRECT>  q >= 1: one warp per observation j, looping over the g
 //                               components; the M lattice points of every T_r are split
 //                               over the 32 lanes and combined by xor-shuffle reductions
-//                               (Alg. 2; formulas DESIGN.md §3).
+//                               (Alg. 2; formulas DESIGN.md §3).  MODE 0
+//                               statistics, 1 density pass (log-likelihood, tau / MAP labels),
+//                               2 per-pair dump; DIRECT = SOV-direct moments (reading D1).
 //   estep_t_mma_kernel<G>       q == 0 (Delta = 0): warp per 32 observations,
 //                               S3 by FP64 tensor-core MMA (default); estep_t_kernel<P> is the
 //                               shared-memory register-blocked variant (CFUST_T_MMA=0).
-//   reduce_kernel               deterministic second pass over per-block partial sums.
-//   mstep_kernel                per-component M-step (Alg. 3; reading R-M).
+//   reduce_kernel               deterministic column sums of the per-block partials.
+//   mstep_kernel, mstep_derive_kernel  one warp per component: M-step (Alg. 3, PAPER.md:370-381;
+//                               reading R-M), then pi and the derived quantities.
 //   derive_kernel               Omega, chol, A, Lambda, constants.
-//   chi_kernel                  chi radius nodes of the lattice for df m0, m0+1, m0+2.
+//   chi_kernel                  chi radius nodes of the lattice for df m0, m0+1, m0+2 (+ log V).
+//   lattice_kernel, check_finite_kernel, special_kernel (diagnostic), dump_t_kernel (q = 0 dump).
+// Alg. 1 (multi-start initialisation) kernels live in cfust_init.cu.
 //
-// No tensor cores: p, q <= 8 and the work is scalar special-function integration, not a
-// dense contraction (BASELINE.json north_star).
+// Tensor cores: only the q = 0 Gram contraction is a dense product (DMMA); everything else is
+// scalar FP64 special-function integration (BASELINE.json north_star).
 #include "cfust_device.cuh"
 #include "cfust_internal.h"
 
