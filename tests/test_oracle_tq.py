@@ -54,6 +54,33 @@ def test_chi_table_vs_scipy(orc):
         assert np.max(np.abs(tab / ref - 1)) < 1e-13
 
 
+def test_logchi_table_vs_scipy(orc):
+    """log V_l = log chi2_m^{-1}(w_l) (exact e1, reading R2') against scipy's quantile, absolute
+    error (log V can be ~0)."""
+    lat = _lat(orc, 1024)
+    for m in [3.5, 9.2, 26.0]:
+        lv = orc.logchi_table(lat, m)
+        w = np.array([orc.lattice_w(lat, l, 0) for l in range(lat.M)])
+        assert np.max(np.abs(lv - np.log(st.chi2.ppf(w, m)))) < 1e-12
+
+
+def test_Tr_w_consistent_with_Tr(orc):
+    """The weighted lattice rule returns the same T as the plain one and, with lv = 1 everywhere,
+    wsum = T (the weights enter only the second sum)."""
+    import ctypes as C
+    lat = _lat(orc, 2048)
+    b = np.array([0.3, -0.2, 0.9])
+    S = np.array([[1.0, 0.3, 0.1], [0.3, 1.2, -0.2], [0.1, -0.2, 0.8]])
+    m = 7.5
+    chi = orc.chi_table(lat, m)
+    T = orc.Tr(b, S, m, lat, chi)
+    ones = np.ones(lat.M)
+    ws = np.zeros(1)
+    gap = np.array([np.inf])
+    Tw = orc.lib().orc_Tr_w(3, orc._p(b), orc._p(S), m, lat.ptr, orc._p(chi), orc._p(ones), orc._p(gap), orc._p(ws))
+    assert Tw == T and abs(ws[0] - T) <= 1e-15
+
+
 def test_T0_T1_closed(orc):
     assert orc.Tr(np.zeros(0), np.zeros((0, 0)), 5.0) == 1.0
     for b, s, m in [(0.4, 2.0, 5.3), (-3.0, 0.7, 11.0)]:
