@@ -61,8 +61,10 @@ typedef struct {
     double nu_lo, nu_hi;           /* nu bracket; 0,0 -> [0.1, 1000] (reading A7)                 */
     int32_t y_on_device;           /* 1: y is a caller-owned device pointer (not copied)          */
     int32_t device;                /* CUDA device ordinal; < 0 -> current device                  */
-    int32_t rank, world;           /* world <= 1: single GPU, no NCCL                              */
-    const void *nccl_id;           /* 128-byte ncclUniqueId, identical on all ranks (world > 1)    */
+    int32_t rank, world;           /* world <= 1: single GPU (no NCCL unless nccl_id is given)     */
+    const void *nccl_id;           /* 128-byte ncclUniqueId, identical on all ranks; required when
+                                      world > 1; with world = 1 it creates a one-rank communicator
+                                      so every collective path runs (tests)                       */
     int64_t n_total;               /* sum of n over ranks (pi = S0 / n_total); 0 -> n              */
     int32_t timing;                /* 1: record CUDA events per phase (see cfust_get_timing)       */
     int32_t e1_exact;              /* 0: e1 = E[log W|y] by the closed-form approximation (reading

@@ -150,7 +150,7 @@ int reset_status(cfust_ctx *ctx) {
 // world > 1: max-reduce the status word over ranks (status[0] underflow flag, status[1] negative
 // error codes -> reduced as max of -code, status[2] non-finite y) so that all ranks agree.
 int global_status(cfust_ctx *ctx) {
-    if (ctx->world <= 1) return CFUST_OK;
+    if (!ctx->comm) return CFUST_OK;
     NC(ncclAllReduce(ctx->s.status, ctx->s.status, 1, ncclInt32, ncclMax, ctx->comm, ctx->stream));
     NC(ncclAllReduce(ctx->s.status + 1, ctx->s.status + 1, 1, ncclInt32, ncclMin, ctx->comm, ctx->stream));
     NC(ncclAllReduce(ctx->s.status + 2, ctx->s.status + 2, 1, ncclInt32, ncclMax, ctx->comm, ctx->stream));
@@ -169,7 +169,7 @@ int enqueue_estep(cfust_ctx *ctx, int mode) {
     ctx->launches += 1;
     rec(ctx, 2);
     ctx->nblocks_last = nb;
-    if (ctx->world > 1) {
+    if (ctx->comm) {
         const size_t len = (mode == 1) ? 1 : size_t(s.g) * s.K + 1;
         NC(ncclAllReduce(mode == 1 ? ctx->d_ll : s.stats, mode == 1 ? ctx->d_ll : s.stats, len, ncclDouble, ncclSum,
                          ctx->comm, ctx->stream));
@@ -348,8 +348,8 @@ int cfust_em_init(cfust_ctx **out, const double *y, int64_t n, int32_t p, int32_
         // Multi-rank: the communicator is created BEFORE the validation verdict, and the status word
         // (non-finite y, derive errors) is max-reduced over ranks, so every rank returns the same
         // code — a rank failing alone would leave the others blocked in the next collective.
-        if (ctx->world > 1) {
-            if (!opts->nccl_id) { rc = fail(ctx, CFUST_EINVAL, "world > 1 needs nccl_id"); break; }
+        if (ctx->world > 1 && !opts->nccl_id) { rc = fail(ctx, CFUST_EINVAL, "world > 1 needs nccl_id"); break; }
+        if (opts->nccl_id) {   // (world = 1 with an id: a one-rank communicator, every collective path live)
             ncclUniqueId id;
             std::memcpy(&id, opts->nccl_id, sizeof(id));
             ncclResult_t r = ncclCommInitRank(&ctx->comm, ctx->world, id, ctx->rank);
@@ -652,7 +652,7 @@ int sync_ctx(cfust_ctx *ctx) {
 }
 
 int allreduce_sum(cfust_ctx *ctx, double *buf, size_t len) {
-    if (ctx->world > 1) NC(ncclAllReduce(buf, buf, len, ncclDouble, ncclSum, ctx->comm, ctx->stream));
+    if (ctx->comm) NC(ncclAllReduce(buf, buf, len, ncclDouble, ncclSum, ctx->comm, ctx->stream));
     return CFUST_OK;
 }
 
@@ -674,7 +674,7 @@ int global_argmax(cfust_ctx *ctx, const InitWS &w, double *val, int64_t *idx) {
     const DevState &s = ctx->s;
     CUI(launch_argmax(w.mind, s.n, ctx->j0, w.scratch, w.amax, ctx->stream));
     ctx->launches += 2;
-    if (ctx->world > 1) {
+    if (ctx->comm) {
         NC(ncclAllGather(w.amax, w.gath, 2, ncclDouble, ctx->comm, ctx->stream));
         CU(cudaMemcpyAsync(ctx->h_ipin, w.gath, sizeof(double) * 2 * ctx->world, cudaMemcpyDeviceToHost, ctx->stream));
     } else {
