@@ -127,7 +127,7 @@ __device__ __forceinline__ double dev_n1_logpdf0(double loc, double s2) {
 }
 
 // Regularized incomplete gamma: series for P (x < a + 1), Legendre CF for Q otherwise.
-__device__ inline double dev_gamma_series_P(double a, double x) {
+__device__ inline double dev_gamma_series_P(double a, double x, double lga) {
     double sum = 1.0 / a, term = sum, ap = a;
     for (int k = 0; k < 10000; ++k) {
         ap += 1.0;
@@ -135,9 +135,9 @@ __device__ inline double dev_gamma_series_P(double a, double x) {
         sum += term;
         if (fabs(term) <= fabs(sum) * 1e-17) break;
     }
-    return sum * exp(a * log(x) - x - lgamma(a));
+    return sum * exp(a * log(x) - x - lga);
 }
-__device__ inline double dev_gamma_cf_Q(double a, double x) {
+__device__ inline double dev_gamma_cf_Q(double a, double x, double lga) {
     const double fpmin = 1e-300;
     double b = x + 1.0 - a, c = 1.0 / fpmin, d = 1.0 / b, h = d;
     for (int k = 1; k < 10000; ++k) {
@@ -150,15 +150,15 @@ __device__ inline double dev_gamma_cf_Q(double a, double x) {
         h *= del;
         if (fabs(del - 1.0) <= 1e-16) break;
     }
-    return exp(a * log(x) - x - lgamma(a)) * h;
+    return exp(a * log(x) - x - lga) * h;
 }
-// log P(a,x) (upper = 0) or log Q(a,x) (upper = 1)
-__device__ inline double dev_log_gamma_PQ(double a, double x, int upper) {
+// log P(a,x) (upper = 0) or log Q(a,x) (upper = 1); lga = lgamma(a) (computed once by the caller)
+__device__ inline double dev_log_gamma_PQ(double a, double x, int upper, double lga) {
     if (x < a + 1.0) {
-        const double P = dev_gamma_series_P(a, x);
+        const double P = dev_gamma_series_P(a, x, lga);
         return upper ? log1p(-P) : log(P);
     }
-    const double Q = dev_gamma_cf_Q(a, x);
+    const double Q = dev_gamma_cf_Q(a, x, lga);
     return upper ? log(Q) : log1p(-Q);
 }
 
@@ -166,6 +166,7 @@ __device__ inline double dev_log_gamma_PQ(double a, double x, int upper) {
 // Newton on log F in s = log(v/2), bracketed; Wilson-Hilferty start.
 __device__ inline double dev_chi2_quantile(double w, double m) {
     const double a = 0.5 * m;
+    const double lga = lgamma(a);
     const int upper = (w > 0.5);
     const double ltarget = log(upper ? (1.0 - w) : w);
     const double zq = Phiinv(w);
@@ -173,24 +174,24 @@ __device__ inline double dev_chi2_quantile(double w, double m) {
     double v = m * pow(fmax(1.0 - h9 + zq * sqrt(h9), 1e-3), 3.0);
     double s = log(0.5 * v);
     // small-v regime: P ~ x^a / Gamma(a+1)
-    const double s_small = (log(w) + lgamma(a + 1.0)) / a;
+    const double s_small = (log(w) + lga + log(a)) / a;   // lgamma(a+1) = lgamma(a) + log(a)
     if (!upper && s_small < s) s = s_small;
     double lo = -745.0, hi = fmax(0.0, log(a)) + 1.0;
     for (int k = 0; k < 100; ++k) {   // make sure hi brackets from above
-        const double g = dev_log_gamma_PQ(a, exp(hi), upper) - ltarget;
+        const double g = dev_log_gamma_PQ(a, exp(hi), upper, lga) - ltarget;
         if (upper ? (g < 0.0) : (g > 0.0)) break;
         hi += 1.0;
     }
     if (!(s > lo && s < hi)) s = 0.5 * (lo + hi);
     for (int it = 0; it < 300; ++it) {
         const double x = exp(s);
-        const double lF = dev_log_gamma_PQ(a, x, upper);
+        const double lF = dev_log_gamma_PQ(a, x, upper, lga);
         const double g = lF - ltarget;
         if (g == 0.0) break;
         const bool root_below = upper ? (g < 0.0) : (g > 0.0);
         if (root_below) hi = s; else lo = s;
         // d log F / ds = x f(x) / F, f the Gamma(a,1) density; negative for Q
-        const double ldens = a * log(x) - x - lgamma(a);
+        const double ldens = a * log(x) - x - lga;
         double dg = exp(ldens - lF);
         if (upper) dg = -dg;
         double sn = s - g / dg;
