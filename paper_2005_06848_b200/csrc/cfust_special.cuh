@@ -62,11 +62,51 @@ __device__ __forceinline__ double div_fast(double p, double q) {
 #define CFUST_OWN_ELEM 1   // own branch-free exp/log/sqrt; with the seeded Phi^{-1} 11% faster E-step
 #endif                     // than libdevice (profiles/r01_seed_variants.log)
 
+#ifndef CFUST_EXP_TAB
+#define CFUST_EXP_TAB 0
+#endif
+
+#if CFUST_EXP_TAB
+// 2^(j/64), j = 0..63, correctly rounded (mpmath, 200 bits); read through L1 (__ldg): a
+// divergent index would serialise a constant-bank load.
+__device__ const double g_EXP2J[64] = {
+    0x1.0000000000000p+0, 0x1.02c9a3e778061p+0, 0x1.059b0d3158574p+0, 0x1.0874518759bc8p+0,
+    0x1.0b5586cf9890fp+0, 0x1.0e3ec32d3d1a2p+0, 0x1.11301d0125b51p+0, 0x1.1429aaea92de0p+0,
+    0x1.172b83c7d517bp+0, 0x1.1a35beb6fcb75p+0, 0x1.1d4873168b9aap+0, 0x1.2063b88628cd6p+0,
+    0x1.2387a6e756238p+0, 0x1.26b4565e27cddp+0, 0x1.29e9df51fdee1p+0, 0x1.2d285a6e4030bp+0,
+    0x1.306fe0a31b715p+0, 0x1.33c08b26416ffp+0, 0x1.371a7373aa9cbp+0, 0x1.3a7db34e59ff7p+0,
+    0x1.3dea64c123422p+0, 0x1.4160a21f72e2ap+0, 0x1.44e086061892dp+0, 0x1.486a2b5c13cd0p+0,
+    0x1.4bfdad5362a27p+0, 0x1.4f9b2769d2ca7p+0, 0x1.5342b569d4f82p+0, 0x1.56f4736b527dap+0,
+    0x1.5ab07dd485429p+0, 0x1.5e76f15ad2148p+0, 0x1.6247eb03a5585p+0, 0x1.6623882552225p+0,
+    0x1.6a09e667f3bcdp+0, 0x1.6dfb23c651a2fp+0, 0x1.71f75e8ec5f74p+0, 0x1.75feb564267c9p+0,
+    0x1.7a11473eb0187p+0, 0x1.7e2f336cf4e62p+0, 0x1.82589994cce13p+0, 0x1.868d99b4492edp+0,
+    0x1.8ace5422aa0dbp+0, 0x1.8f1ae99157736p+0, 0x1.93737b0cdc5e5p+0, 0x1.97d829fde4e50p+0,
+    0x1.9c49182a3f090p+0, 0x1.a0c667b5de565p+0, 0x1.a5503b23e255dp+0, 0x1.a9e6b5579fdbfp+0,
+    0x1.ae89f995ad3adp+0, 0x1.b33a2b84f15fbp+0, 0x1.b7f76f2fb5e47p+0, 0x1.bcc1e904bc1d2p+0,
+    0x1.c199bdd85529cp+0, 0x1.c67f12e57d14bp+0, 0x1.cb720dcef9069p+0, 0x1.d072d4a07897cp+0,
+    0x1.d5818dcfba487p+0, 0x1.da9e603db3285p+0, 0x1.dfc97337b9b5fp+0, 0x1.e502ee78b3ff6p+0,
+    0x1.ea4afa2a490dap+0, 0x1.efa1bee615a27p+0, 0x1.f50765b6e4540p+0, 0x1.fa7c1819e90d8p+0,
+};
+#endif
+
 // exp(x) for x <= 709 (x >= -708 exact to ~1 ulp; below: 0, i.e. results < 1e-307 flush).
-// x = k ln2 + r, |r| <= ln2/2: k from the 1.5*2^52 rounding trick, r with a two-part ln2,
-// Taylor to r^13, 2^k by adding k to the exponent field.
+// Default: x = k ln2 + r, |r| <= ln2/2: k from the 1.5*2^52 rounding trick, r with a two-part
+// ln2, Taylor to r^13, 2^k by adding k to the exponent field.
+// CFUST_EXP_TAB: x = (64 m + j) ln2/64 + r, |r| <= ln2/128: exp = 2^m 2^(j/64) (1 + q(r)),
+// q = r + ... + r^5/120 (truncation r^6/720 < 4e-17), 2^(j/64) from a 64-entry table:
+// 10 FP64 operations instead of 17.
 __device__ __forceinline__ double exp_neg(double x) {
-#if CFUST_OWN_ELEM
+#if CFUST_OWN_ELEM && CFUST_EXP_TAB
+    const double t = fma(x, 92.33248261689366, 6755399441055744.0);
+    const int k = __double2loint(t);
+    const double kd = t - 6755399441055744.0;
+    const double r = fma(kd, -3.623510646634843e-19, fma(kd, -0.010830424696249145, x));
+    const double q = r * fma(r, fma(r, fma(r, fma(r, 1.0 / 120.0, 1.0 / 24.0), 1.0 / 6.0), 0.5), 1.0);
+    const double T = __ldg(&g_EXP2J[k & 63]);
+    const double p = fma(T, q, T);
+    const double res = __hiloint2double(__double2hiint(p) + (k >> 6) * (1 << 20), __double2loint(p));
+    return (x < -708.0) ? 0.0 : res;
+#elif CFUST_OWN_ELEM
     const double t = fma(x, 1.4426950408889634074, 6755399441055744.0);
     const int k = __double2loint(t);
     const double kd = t - 6755399441055744.0;
