@@ -954,11 +954,11 @@ __global__ void __launch_bounds__(TT, 2) estep_t_kernel(EArgs A, int mode) {
 #define CFUST_T_MMA 1
 #endif
 #ifndef CFUST_TW
-#define CFUST_TW 8
+#define CFUST_TW 16
 #endif
 constexpr int TW = CFUST_TW;   // warps per block of the q = 0 kernel
 #ifndef CFUST_T_MB
-#define CFUST_T_MB 2        // blocks per SM (G = 5 spills ~300 B but runs 15% faster than 1 block, profiles/r01_cfg3_mma.log)
+#define CFUST_T_MB 1        // blocks per SM: 16 warps in one block (profiles/r01_cfg3_mma.log)
 #endif
 
 __device__ __forceinline__ void dmma_884(double &c0, double &c1, double a, double b) {
@@ -977,6 +977,36 @@ __global__ void __launch_bounds__(TW * 32, CFUST_T_MB) estep_t_mma_kernel(EArgs 
     for (int t = threadIdx.x; t < G * int(sizeof(CompDev) / sizeof(double)); t += blockDim.x)
         reinterpret_cast<double *>(comp)[t] = reinterpret_cast<const double *>(A.comp)[t];
     for (int t = threadIdx.x; t < TW * (GK + 1); t += blockDim.x) red[t] = 0.0;
+    // L_i^{-1} (lower, row-major, stride PMAX; rows/columns >= p zero) column by column, then
+    // m_i = L_i^{-1} mu_i, so that v = L^{-1}(y - mu) = L^{-1} y - m has rows independent of each
+    // other (no substitution chain: 9 % faster at cfg3, profiles/r01_cfg3_mma.log).
+    double *Li = red + TW * (GK + 1);                    // [G][PMAX*PMAX]
+    double *mL = Li + G * PMAX * PMAX;                   // [G][PMAX]
+    __syncthreads();
+    for (int t = threadIdx.x; t < G * PMAX; t += blockDim.x) {
+        const int i = t / PMAX, b = t % PMAX;
+        const CompDev &cp = comp[i];
+        double *X = Li + i * PMAX * PMAX;
+        for (int a = 0; a < PMAX; ++a) {
+            double x = 0.0;
+            if (a < p && b < p && a >= b) {
+                if (a == b) x = cp.Linv[a];
+                else {
+                    double r = 0.0;
+                    for (int c = b; c < a; ++c) r = fma(cp.L[a * PMAX + c], X[c * PMAX + b], r);
+                    x = -r * cp.Linv[a];
+                }
+            }
+            X[a * PMAX + b] = x;
+        }
+    }
+    __syncthreads();
+    for (int t = threadIdx.x; t < G * PMAX; t += blockDim.x) {
+        const int i = t / PMAX, a = t % PMAX;
+        double m = 0.0;
+        for (int b = 0; b <= a && b < p; ++b) m = fma(Li[i * PMAX * PMAX + a * PMAX + b], comp[i].mu[b], m);
+        mL[t] = m;
+    }
     __syncthreads();
     const bool nrm = A.family == 1;
     double s0[G], s1[G], s7[G], s2[G], c0[G], c1[G];
@@ -990,23 +1020,32 @@ __global__ void __launch_bounds__(TW * 32, CFUST_T_MB) estep_t_mma_kernel(EArgs 
         const int64_t j = tile * 32 + lane;
         const bool valid = j < n;
         double y[PMAX];
+        if (p == PMAX) {   // 64-byte rows: four 16-byte loads per lane
 #pragma unroll
-        for (int a = 0; a < PMAX; ++a) y[a] = (valid && a < p) ? __ldg(A.y + j * p + a) : 0.0;
+            for (int a = 0; a < PMAX; a += 2) {
+                const double2 v2 = valid ? __ldg(reinterpret_cast<const double2 *>(A.y + j * PMAX + a)) : make_double2(0.0, 0.0);
+                y[a] = v2.x;
+                y[a + 1] = v2.y;
+            }
+        } else {
+#pragma unroll
+            for (int a = 0; a < PMAX; ++a) y[a] = (valid && a < p) ? __ldg(A.y + j * p + a) : 0.0;
+        }
         double lf[G], dd[G], l1[G];
         double mx = -CUDART_INF;
 #pragma unroll
         for (int i = 0; i < G; ++i) {
             const CompDev &cp = comp[i];
-            double v[PMAX], d = 0.0;
+            double d = 0.0;
+            // all PMAX rows, no branch on p: rows >= p of L^{-1} and m are zero and y[a >= p] = 0, so the
+            // padded rows add exactly 0 — and the scheduler interleaves rows and components (9 %)
+            const double *Lr = Li + i * PMAX * PMAX, *mr = mL + i * PMAX;
 #pragma unroll
             for (int a = 0; a < PMAX; ++a) {
-                if (a < p) {
-                    double t = y[a] - cp.mu[a];
+                double t = -mr[a];
 #pragma unroll
-                    for (int b = 0; b < a; ++b) t = fma(-cp.L[a * PMAX + b], v[b], t);
-                    v[a] = t * cp.Linv[a];
-                    d = fma(v[a], v[a], d);
-                }
+                for (int b = 0; b <= a; ++b) t = fma(Lr[a * PMAX + b], y[b], t);
+                d = fma(t, t, d);
             }
             dd[i] = d;
             l1[i] = nrm ? 0.0 : log1p_pos(d * cp.inv_nu);
@@ -1593,7 +1632,8 @@ static int launch_cfust_mode(const DevState &s, EArgs &a, cudaStream_t st, int *
 template <int G>
 static int launch_t_mma_g(const DevState &s, EArgs &a, int mode, cudaStream_t st, int *nb) {
     auto kern = estep_t_mma_kernel<G>;
-    const size_t sm = sizeof(CompDev) * G + sizeof(double) * TW * (size_t(G) * s.K + 1);
+    const size_t sm = sizeof(CompDev) * G + sizeof(double) * TW * (size_t(G) * s.K + 1)
+                      + sizeof(double) * G * (PMAX * PMAX + PMAX);   // L^{-1}, m
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
     if (e != cudaSuccess) return int(e);
     int per_sm = 0;
