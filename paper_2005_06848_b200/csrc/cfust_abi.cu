@@ -6,6 +6,12 @@
 #include "cfust_internal.h"
 
 #include <nccl.h>
+#ifndef CFUST_NVTX
+#define CFUST_NVTX 1
+#endif
+#if CFUST_NVTX
+#include <nvtx3/nvToolsExt.h>   // header-only NVTX v3: ranges cost a pointer test unless a tool attaches
+#endif
 
 #include <chrono>
 #include <cmath>
@@ -46,6 +52,25 @@ struct cfust_ctx {
 };
 
 namespace {
+
+// NVTX ranges (SURVEY §5 tracing): one per C-ABI call and per phase of an iteration, so an nsys /
+// ncu --nvtx timeline attributes kernels to E-step, reduction, all-reduce and M-step.
+struct Nvtx {
+    explicit Nvtx(const char *name) {
+#if CFUST_NVTX
+        nvtxRangePushA(name);
+#else
+        (void)name;
+#endif
+    }
+    ~Nvtx() {
+#if CFUST_NVTX
+        nvtxRangePop();
+#endif
+    }
+    Nvtx(const Nvtx &) = delete;
+    Nvtx &operator=(const Nvtx &) = delete;
+};
 
 int fail(cfust_ctx *c, int code, const std::string &msg) {
     if (c) c->err = msg;
@@ -162,14 +187,21 @@ int enqueue_estep(cfust_ctx *ctx, int mode) {
     DevState &s = ctx->s;
     int nb = 0;
     rec(ctx, 0);
-    CUI(launch_estep(s, mode, nullptr, 0, nullptr, ctx->stream, &nb));
+    {
+        Nvtx r(mode == 1 ? "cfust:loglik-kernel" : "cfust:estep-kernel");
+        CUI(launch_estep(s, mode, nullptr, 0, nullptr, ctx->stream, &nb));
+    }
     ctx->launches += 1;
     rec(ctx, 1);
-    CUI(launch_reduce(s, nb, mode, mode == 1 ? ctx->d_ll : s.stats, ctx->stream));
+    {
+        Nvtx r("cfust:reduce");
+        CUI(launch_reduce(s, nb, mode, mode == 1 ? ctx->d_ll : s.stats, ctx->stream));
+    }
     ctx->launches += 1;
     rec(ctx, 2);
     ctx->nblocks_last = nb;
     if (ctx->comm) {
+        Nvtx r("cfust:allreduce");
         const size_t len = (mode == 1) ? 1 : size_t(s.g) * s.K + 1;
         NC(ncclAllReduce(mode == 1 ? ctx->d_ll : s.stats, mode == 1 ? ctx->d_ll : s.stats, len, ncclDouble, ncclSum,
                          ctx->comm, ctx->stream));
@@ -181,6 +213,7 @@ int enqueue_estep(cfust_ctx *ctx, int mode) {
 }
 
 int enqueue_mstep(cfust_ctx *ctx) {
+    Nvtx r("cfust:mstep");
     CUI(launch_mstep(ctx->s, ctx->stream));
     CUI(launch_chi(ctx->s, ctx->stream));
     ctx->launches += (ctx->s.M > 0) ? 3 : 2;   // M-step, pi + derive, chi nodes
@@ -242,6 +275,7 @@ void cfust_destroy(cfust_ctx *ctx) {
 
 int cfust_em_init(cfust_ctx **out, const double *y, int64_t n, int32_t p, int32_t g, int32_t q,
                   const cfust_params *init, const cfust_opts *opts) {
+    Nvtx nvtx_range("cfust_em_init");
     if (!out) return CFUST_EINVAL;
     *out = nullptr;
     cfust_ctx *ctx = new cfust_ctx();
@@ -384,6 +418,7 @@ int cfust_set_data(cfust_ctx *ctx, const double *y, int32_t on_device) {
 }
 
 int cfust_estep(cfust_ctx *ctx, double *loglik_out, double *stats_out) {
+    Nvtx nvtx_range("cfust_estep");
     if (!ctx) return CFUST_EINVAL;
     CU(cudaSetDevice(ctx->device));
     DevState &s = ctx->s;
@@ -405,6 +440,7 @@ int cfust_estep(cfust_ctx *ctx, double *loglik_out, double *stats_out) {
 }
 
 int cfust_mstep(cfust_ctx *ctx) {
+    Nvtx nvtx_range("cfust_mstep");
     if (!ctx) return CFUST_EINVAL;
     if (!ctx->have_stats) return fail(ctx, CFUST_EINVAL, "cfust_mstep needs a preceding cfust_estep");
     CU(cudaSetDevice(ctx->device));
@@ -420,6 +456,7 @@ int cfust_mstep(cfust_ctx *ctx) {
 }
 
 int cfust_iterate(cfust_ctx *ctx, double *loglik_out) {
+    Nvtx nvtx_range("cfust_iterate");
     if (!ctx) return CFUST_EINVAL;
     CU(cudaSetDevice(ctx->device));
     DevState &s = ctx->s;
@@ -444,6 +481,7 @@ int cfust_iterate(cfust_ctx *ctx, double *loglik_out) {
 }
 
 int cfust_loglik(cfust_ctx *ctx, double *out) {
+    Nvtx nvtx_range("cfust_loglik");
     if (!ctx || !out) return CFUST_EINVAL;
     CU(cudaSetDevice(ctx->device));
     int rc = reset_status(ctx);
@@ -458,6 +496,7 @@ int cfust_loglik(cfust_ctx *ctx, double *out) {
 }
 
 int cfust_predict(cfust_ctx *ctx, int32_t *labels_out, double *tau_out, double *loglik_out) {
+    Nvtx nvtx_range("cfust_predict");
     if (!ctx) return CFUST_EINVAL;
     DevState &s = ctx->s;
     CU(cudaSetDevice(ctx->device));
@@ -494,6 +533,7 @@ static int aitken_stop(double l2, double l1, double l0, double tol) {
 }
 
 int cfust_fit(cfust_ctx *ctx, int32_t max_iter, double tol, cfust_result *out) {
+    Nvtx nvtx_range("cfust_fit");
     if (!ctx || !out || max_iter < 0) return CFUST_EINVAL;
     if (out->loglik_trace && out->trace_cap < max_iter + 1) return fail(ctx, CFUST_EINVAL, "trace_cap < max_iter + 1");
     const auto t0 = std::chrono::steady_clock::now();
@@ -780,6 +820,7 @@ int random_partition(cfust_ctx *ctx, uint64_t seed, int l, int m, int32_t *lab) 
 }  // namespace
 
 int cfust_init_partitions(cfust_ctx *ctx, int32_t m, uint64_t seed, int32_t kmeans_iters, int32_t *labels_out) {
+    Nvtx nvtx_range("cfust_init_partitions");
     if (!ctx || m < 1 || kmeans_iters < 0) return CFUST_EINVAL;
     DevState &s = ctx->s;
     if (s.n_total < double(s.g)) return fail(ctx, CFUST_EINVAL, "n_total < g");
@@ -798,6 +839,7 @@ int cfust_init_partitions(cfust_ctx *ctx, int32_t m, uint64_t seed, int32_t kmea
 
 int cfust_init_select(cfust_ctx *ctx, int32_t m, const int32_t *labels, int32_t burn_in, double *loglik0_out,
                       int32_t *best_out) {
+    Nvtx nvtx_range("cfust_init_select");
     if (!ctx || m < 1 || burn_in < 0) return CFUST_EINVAL;
     DevState &s = ctx->s;
     if (!labels && m > ctx->m_cap) return fail(ctx, CFUST_EINVAL, "no partitions: call cfust_init_partitions first");
