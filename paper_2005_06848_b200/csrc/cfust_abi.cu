@@ -16,6 +16,7 @@
 #include <chrono>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -338,6 +339,11 @@ int cfust_em_init(cfust_ctx **out, const double *y, int64_t n, int32_t p, int32_
         s.family = opts->family;
         s.direct = direct ? 1 : 0;
         s.nw = nz;
+        {   // CFUST_SPLIT=1|2|4|8: force the warps-per-observation of the small-n statistics pass (tests)
+            const char *sp = std::getenv("CFUST_SPLIT");
+            const int v = sp ? std::atoi(sp) : 0;
+            s.split_force = (v == 1 || v == 2 || v == 4 || v == 8) ? v : 0;
+        }
         s.num_sms = prop.multiProcessorCount;
         const int GK1 = g * s.K + 1;
         auto alloc = [&](void **ptr, size_t bytes) { return cudaMalloc(ptr, bytes < 8 ? 8 : bytes) == cudaSuccess; };

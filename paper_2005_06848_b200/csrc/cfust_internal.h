@@ -32,6 +32,7 @@ struct DevState {
     int family;                     // 0: skew-t (CFUST); 1: skew-normal (CFUSN, nu = inf; q = 0: Gaussian)
     int direct;                     // 1: SOV-direct truncated moments (reading D1); 0: analytic (O6-O7)
     int nw;                         // lattice coordinates tabulated in W (rows)
+    int split_force;                // warps per observation for small n: 0 auto, 1/2/4/8 forced (env CFUST_SPLIT)
     double *tau_out;                // density pass (mode 1): responsibilities [n][g] if non-NULL
     int32_t *label_out;             // density pass (mode 1): argmax_i tau_ij [n] if non-NULL
 };

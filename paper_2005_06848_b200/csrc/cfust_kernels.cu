@@ -110,18 +110,22 @@ struct Tune {
 };
 
 // WT: also accumulate *wacc += f_l lv_l (exact e1, reading R2': lv = log V node table).
-template <int R, int NPTS, bool WT = false>
+// SPLIT warps share one observation (small n): warp sub = wid % SPLIT takes the point blocks
+// sub, sub + SPLIT, ... of 32 * NPTS points; split_sum combines the SPLIT warp totals.
+template <int R, int NPTS, bool WT = false, int SPLIT = 1>
 __device__ __forceinline__ double sov_lane_sum(const double (&binv)[R], const double (&Cn)[R * (R - 1) / 2],
                                                const double *__restrict__ chi, const double *__restrict__ W, int M,
                                                int lane, const double *__restrict__ lv = nullptr,
                                                double *wacc = nullptr) {
     // NPTS lattice points per iteration (l, l + 32, ...): independent chains for the FP64 pipe.
-    // M is a power of two >= 1024, so 32 * NPTS divides it exactly when NPTS is a power of two.
+    // M is a power of two >= 1024, so 32 * NPTS * SPLIT divides it exactly (powers of two, <= 32).
     static_assert(NPTS == 1 || NPTS == 2 || NPTS == 4, "NPTS must divide M / 32");
+    static_assert(NPTS * SPLIT <= 32, "32 * NPTS * SPLIT must divide M >= 1024");
     double acc[NPTS], accw[NPTS];
 #pragma unroll
     for (int j = 0; j < NPTS; ++j) acc[j] = accw[j] = 0.0;
-    for (int l0 = lane; l0 < M; l0 += 32 * NPTS) {
+    const int sub = (SPLIT > 1) ? int(threadIdx.x >> 5) % SPLIT : 0;
+    for (int l0 = lane + sub * 32 * NPTS; l0 < M; l0 += 32 * NPTS * SPLIT) {
         double s[NPTS], e[NPTS], f[NPTS], z[NPTS][R - 1];
 #pragma unroll
         for (int j = 0; j < NPTS; ++j) {
@@ -194,9 +198,31 @@ __device__ __forceinline__ bool sov_setup(const double *b, const double *S, int 
     return true;
 }
 
+// Sum of a warp-uniform value over the SPLIT warps of an observation group (named barrier 1 + group,
+// fixed summation order: every warp of the group gets the same bits, so all take the same branches).
+__device__ __forceinline__ void named_bar(int id, int nthreads) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+template <int SPLIT>
+__device__ __forceinline__ double split_sum(double v) {
+    if constexpr (SPLIT == 1) {
+        return v;
+    } else {
+        __shared__ double part[EW];
+        const int wid = threadIdx.x >> 5, g0 = wid - wid % SPLIT, bar = 1 + wid / SPLIT;
+        if ((threadIdx.x & 31) == 0) part[wid] = v;
+        named_bar(bar, SPLIT * 32);
+        double t = 0.0;
+#pragma unroll
+        for (int k = 0; k < SPLIT; ++k) t += part[g0 + k];
+        named_bar(bar, SPLIT * 32);   // the slots are reused by the next call
+        return t;
+    }
+}
+
 // T_R(b; 0, S, m): R = 0 -> 1; R = 1 -> univariate t CDF; R >= 2 -> lattice rule with
 // univariate-prioritisation reordering (ascending b_k / sqrt(S_kk), stable; reading A13).
-template <int R, int NP>
+template <int R, int NP, int SPLIT = 1>
 __device__ __noinline__ double T_eval(const double *b, const double *S, int lds, double m,
                                       const double *__restrict__ chi, const double *__restrict__ W, int M,
                                       int lane) {
@@ -207,14 +233,14 @@ __device__ __noinline__ double T_eval(const double *b, const double *S, int lds,
     } else {
         double binv[R], Cn[R * (R - 1) / 2];
         if (!sov_setup<R>(b, S, lds, binv, Cn)) return CUDART_NAN;
-        const double acc = sov_lane_sum<R, NP>(binv, Cn, chi, W, M, lane);
-        return warp_sum(acc) / double(M);
+        const double acc = sov_lane_sum<R, NP, false, SPLIT>(binv, Cn, chi, W, M, lane);
+        return split_sum<SPLIT>(warp_sum(acc)) / double(M);
     }
 }
 
 // T_R on the lattice together with *wsum = (1/M) sum_l f_l lv_l over the same points (exact e1,
 // reading R2'); R = 1 is evaluated on the lattice here too (f_l = Phi(s_l b / sqrt(S))).
-template <int R, int NP>
+template <int R, int NP, int SPLIT = 1>
 __device__ __noinline__ double T_eval_w(const double *b, const double *S, int lds, const double *__restrict__ chi,
                                         const double *__restrict__ lv, const double *__restrict__ W, int M, int lane,
                                         double *wsum) {
@@ -222,7 +248,8 @@ __device__ __noinline__ double T_eval_w(const double *b, const double *S, int ld
     double acc = 0.0, accw = 0.0;
     if constexpr (R == 1) {
         const double bs = b[0] / sqrt(S[0]);
-        for (int l = lane; l < M; l += 32) {
+        const int sub = (SPLIT > 1) ? int(threadIdx.x >> 5) % SPLIT : 0;
+        for (int l = lane + 32 * sub; l < M; l += 32 * SPLIT) {
             const double f = Phi(__ldg(chi + l) * bs);
             acc += f;
             accw = fma(f, __ldg(lv + l), accw);
@@ -230,10 +257,10 @@ __device__ __noinline__ double T_eval_w(const double *b, const double *S, int ld
     } else {
         double binv[R], Cn[R * (R - 1) / 2];
         if (!sov_setup<R>(b, S, lds, binv, Cn)) { *wsum = CUDART_NAN; return CUDART_NAN; }
-        acc = sov_lane_sum<R, NP, true>(binv, Cn, chi, W, M, lane, lv, &accw);
+        acc = sov_lane_sum<R, NP, true, SPLIT>(binv, Cn, chi, W, M, lane, lv, &accw);
     }
-    *wsum = warp_sum(accw) / double(M);
-    return warp_sum(acc) / double(M);
+    *wsum = split_sum<SPLIT>(warp_sum(accw)) / double(M);
+    return split_sum<SPLIT>(warp_sum(acc)) / double(M);
 }
 
 // SOV-direct truncated moments (NEXT-3, reading D1): on T0's own SOV points, the last normal
@@ -394,7 +421,7 @@ __device__ void pair_eval_direct(const CompDev &cp, int p, const double *__restr
 
 // Per pair (observation in ws.y, component cp): O2-O8 of DESIGN.md §3.
 // MODE 1 computes only log f (T0).  Results go to res[] (identical in all lanes).
-template <int Q, int MODE>
+template <int Q, int MODE, int SPLIT = 1>
 __device__ void pair_eval(const CompDev &cp, int p, const double *__restrict__ W, int M, const double *__restrict__ chi,
                           WarpScratch &ws, double *res, int lane, int e1_exact, int family) {
     // family 1 = skew-normal (CFUSN, nu = inf; reading F1): W = 1, normal SOV (radius nodes = 1),
@@ -432,11 +459,11 @@ __device__ void pair_eval(const CompDev &cp, int p, const double *__restrict__ W
     double T0, e1x = 0.0;
     if (MODE != 1 && e1_exact) {   // exact e1 = (sum f lv)/(sum f) - log rho on T0's points (R2')
         double wsum;
-        const double T0lat = T_eval_w<Q, Tune<Q>::NP>(ws.b, cp.Lam, QMAX, chi, chi + CHI_LV * M, W, M, lane, &wsum);
+        const double T0lat = T_eval_w<Q, Tune<Q>::NP, SPLIT>(ws.b, cp.Lam, QMAX, chi, chi + CHI_LV * M, W, M, lane, &wsum);
         T0 = (Q == 1) ? T_eval<1, 1>(ws.b, cp.Lam, QMAX, m0, chi, W, M, lane) : T0lat;   // density: exact T_1
         e1x = wsum / T0lat - log(rho);
     } else {
-        T0 = T_eval<Q, Tune<Q>::NP>(ws.b, cp.Lam, QMAX, mT0, chi, W, M, lane);
+        T0 = T_eval<Q, Tune<Q>::NP, SPLIT>(ws.b, cp.Lam, QMAX, mT0, chi, W, M, lane);
     }
     if (MODE == 1) {
         res[0] = (T0 >= TMIN) ? Q * CUDART_LN2 + logt + log(T0) : -CUDART_INF;
@@ -447,7 +474,7 @@ __device__ void pair_eval(const CompDev &cp, int p, const double *__restrict__ W
         const double sq2 = sqrt((m0 + 2.0) / rho);
 #pragma unroll
         for (int k = 0; k < Q; ++k) ws.b[k] = c[k] * sq2;
-        T2 = T_eval<Q, Tune<Q>::NP>(ws.b, cp.Lam, QMAX, m0 + 2.0, chi + CHI_M2 * M, W, M, lane);
+        T2 = T_eval<Q, Tune<Q>::NP, SPLIT>(ws.b, cp.Lam, QMAX, m0 + 2.0, chi + CHI_M2 * M, W, M, lane);
     }
     res[1] = nrm ? 0.0 : cp.psi_half_m0 - log(0.5 * rho) - m0 / rho;      // e1 - e2, reading A5
     if (!(T0 >= TMIN)) {                                        // reading A16
@@ -508,7 +535,7 @@ __device__ void pair_eval(const CompDev &cp, int p, const double *__restrict__ W
                     }
                     ++ib;
                 }
-                const double val = T_eval<Q2, Tune<Q>::NP>(ws.bc, ws.Sc, QMAX, mT0, chi, W, M, lane);
+                const double val = T_eval<Q2, Tune<Q>::NP, SPLIT>(ws.bc, ws.Sc, QMAX, mT0, chi, W, M, lane);
                 ws.Tkt[k * QMAX + t] = val;
                 ws.Tkt[t * QMAX + k] = val;            // symmetric in {k, t} (A17)
             }
@@ -519,7 +546,7 @@ __device__ void pair_eval(const CompDev &cp, int p, const double *__restrict__ W
     for (int k = 0; k < Q; ++k) {
         double tk = 1.0;
         if constexpr (Q >= 2)
-            tk = T_eval<Q1, Tune<Q>::NP>(ws.ct[k], ws.St[k], QMAX, nrm ? CUDART_INF : m0 + 1.0, chi + CHI_M1 * M, W, M, lane);
+            tk = T_eval<Q1, Tune<Q>::NP, SPLIT>(ws.ct[k], ws.St[k], QMAX, nrm ? CUDART_INF : m0 + 1.0, chi + CHI_M1 * M, W, M, lane);
         ws.Tk[k] = tk;
         h[k] = ws.phi[k] * tk;
     }
@@ -632,8 +659,13 @@ struct EArgs {
 #ifndef CFUST_MBD
 #define CFUST_MBD 2   // resident blocks/SM for the SOV-direct instantiations (profiles/r01_direct_tuning.log)
 #endif
-template <int Q, int MODE, bool DIRECT = false>
+// SPLIT > 1 (analytic statistics and density passes, small n): SPLIT warps per observation, each on 1/SPLIT of the
+// lattice points (sov_lane_sum), totals combined per integral (split_sum); warp 0 of the group
+// accumulates.  The per-pair setup is repeated by the SPLIT warps (identical inputs and bits).
+template <int Q, int MODE, bool DIRECT = false, int SPLIT = 1>
 __global__ void __launch_bounds__(EW * 32, (DIRECT && CFUST_MBD > 0) ? CFUST_MBD : Tune<Q>::MB) estep_cfust_kernel(EArgs A) {
+    static_assert(SPLIT == 1 || (!DIRECT && MODE != 2 && EW % SPLIT == 0), "SPLIT: analytic statistics / density pass only");
+    constexpr int OPB = EW / SPLIT;   // observations per block per sweep
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const int p = A.p, g = A.g, K = A.K, GK = g * K;
@@ -649,10 +681,11 @@ __global__ void __launch_bounds__(EW * 32, (DIRECT && CFUST_MBD > 0) ? CFUST_MBD
     WarpScratch &ws = wsa[wid];
     double *acc = acc_all + wid * (GK + 1);
     const int M = A.M;
-    const int64_t nwarps = int64_t(gridDim.x) * EW;
+    const int64_t ngroups = int64_t(gridDim.x) * OPB;
     const int64_t total = (MODE == 2) ? A.cnt : A.n;
+    const bool lead = (SPLIT == 1) || (wid % SPLIT == 0);   // the warp that accumulates for its group
     double ll = 0.0;
-    for (int64_t jj = int64_t(blockIdx.x) * EW + wid; jj < total; jj += nwarps) {
+    for (int64_t jj = int64_t(blockIdx.x) * OPB + wid / SPLIT; jj < total; jj += ngroups) {
         const int64_t j = (MODE == 2) ? A.idx[jj] : jj;
         __syncwarp();
         if (lane < p) ws.y[lane] = A.y[j * p + lane];
@@ -663,7 +696,7 @@ __global__ void __launch_bounds__(EW * 32, (DIRECT && CFUST_MBD > 0) ? CFUST_MBD
             if constexpr (DIRECT && MODE != 1)
                 pair_eval_direct<Q>(comp[i], p, A.W, M, chi_i, ws, ws.res[i], lane, A.family);
             else
-                pair_eval<Q, MODE == 1 ? 1 : 0>(comp[i], p, A.W, M, chi_i, ws, ws.res[i], lane, A.e1_exact, A.family);
+                pair_eval<Q, MODE == 1 ? 1 : 0, SPLIT>(comp[i], p, A.W, M, chi_i, ws, ws.res[i], lane, A.e1_exact, A.family);
         }
         __syncwarp();
         // Eq. (3)-(4): LSE over components, tau
@@ -672,7 +705,7 @@ __global__ void __launch_bounds__(EW * 32, (DIRECT && CFUST_MBD > 0) ? CFUST_MBD
         for (int i = 0; i < GMAX; ++i)
             if (i < g) { lf[i] = comp[i].logpi + ws.res[i][0]; mx = fmax(mx, lf[i]); }
         if (mx == -CUDART_INF) {
-            if (lane == 0) atomicOr(A.status, 1);
+            if (lane == 0 && lead) atomicOr(A.status, 1);
             continue;
         }
         double se = 0.0;
@@ -680,9 +713,9 @@ __global__ void __launch_bounds__(EW * 32, (DIRECT && CFUST_MBD > 0) ? CFUST_MBD
         for (int i = 0; i < GMAX; ++i)
             if (i < g) se += exp(lf[i] - mx);
         const double lse = mx + log(se);
-        ll += lse;
+        if (lead) ll += lse;
         if constexpr (MODE == 1) {
-            if (A.tau_out && lane == 0) {   // responsibilities and the MAP label (ties -> lowest index)
+            if (A.tau_out && lane == 0 && lead) {   // responsibilities and the MAP label (ties -> lowest index)
                 int best = 0;
                 for (int i = 0; i < g; ++i) {
                     A.tau_out[size_t(j) * g + i] = exp(lf[i] - lse);
@@ -709,6 +742,7 @@ __global__ void __launch_bounds__(EW * 32, (DIRECT && CFUST_MBD > 0) ? CFUST_MBD
             continue;
         }
         // accumulate the eight sufficient statistics (reading A4); lane-owned entries
+        if (!lead) continue;
         for (int e = lane; e < GK; e += 32) {
             const int code = codes[e];
             const int type = code & 15, i = (code >> 4) & 15, a = (code >> 8) & 15, bq = (code >> 12) & 15;
@@ -1583,9 +1617,9 @@ static size_t t_smem(const DevState &s) {
     return sizeof(CompDev) * s.g + sizeof(double) * (size_t(TT) * (YS + 3 * WS) + 32 + tasks);
 }
 
-template <int Q, int MODE, bool DIRECT = false>
+template <int Q, int MODE, bool DIRECT = false, int SPLIT = 1>
 static int launch_cfust_q(const DevState &s, EArgs &a, cudaStream_t st, int *nb) {
-    auto kern = estep_cfust_kernel<Q, MODE, DIRECT>;
+    auto kern = estep_cfust_kernel<Q, MODE, DIRECT, SPLIT>;
     const size_t sm = cfust_smem(s);
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
     if (e != cudaSuccess) return int(e);
@@ -1595,12 +1629,50 @@ static int launch_cfust_q(const DevState &s, EArgs &a, cudaStream_t st, int *nb)
     if (per_sm < 1) per_sm = 1;
     const int64_t work = (MODE == 2) ? a.cnt : a.n;
     int64_t blocks = int64_t(s.num_sms) * per_sm;
-    const int64_t need = (work + EW - 1) / EW;
+    const int64_t need = (work + EW / SPLIT - 1) / (EW / SPLIT);
     if (blocks > need) blocks = need;
     if (blocks < 1) blocks = 1;
     kern<<<int(blocks), EW * 32, sm, st>>>(a);
     *nb = int(blocks);
     return int(cudaGetLastError());
+}
+
+// Warps per observation for the analytic passes at small n: the largest of 1, 2, 4, 8 for which the
+// n * SPLIT observation-warps fit in one wave of resident warps (num_sms x EW x the q-tuned blocks
+// per SM); measured against forced values in profiles/r01_split.log.  s.split_force (env
+// CFUST_SPLIT) overrides.
+static int split_factor(const DevState &s) {
+    if (s.direct) return 1;   // the SOV-direct pass keeps one warp per observation (T0 bits = density pass)
+    if (s.split_force > 0) return s.split_force;
+    const int mb = s.q == 1 ? Tune<1>::MB : s.q == 2 ? Tune<2>::MB : s.q == 3 ? Tune<3>::MB
+                 : s.q == 4 ? Tune<4>::MB : s.q == 5 ? Tune<5>::MB : Tune<6>::MB;
+    const int64_t cap = int64_t(s.num_sms) * EW * mb;
+    int sp = 1;
+    while (sp < 8 && s.n * (sp * 2) <= cap) sp *= 2;
+    return sp;
+}
+
+template <int MODE, int SPLIT>
+static int launch_cfust_split_q(const DevState &s, EArgs &a, cudaStream_t st, int *nb) {
+    switch (s.q) {
+        case 1: return launch_cfust_q<1, MODE, false, SPLIT>(s, a, st, nb);
+        case 2: return launch_cfust_q<2, MODE, false, SPLIT>(s, a, st, nb);
+        case 3: return launch_cfust_q<3, MODE, false, SPLIT>(s, a, st, nb);
+        case 4: return launch_cfust_q<4, MODE, false, SPLIT>(s, a, st, nb);
+        case 5: return launch_cfust_q<5, MODE, false, SPLIT>(s, a, st, nb);
+        case 6: return launch_cfust_q<6, MODE, false, SPLIT>(s, a, st, nb);
+        default: return int(cudaErrorInvalidValue);
+    }
+}
+
+template <int MODE>
+static int launch_cfust_split(const DevState &s, EArgs &a, cudaStream_t st, int *nb, int sp) {
+    switch (sp) {
+        case 2: return launch_cfust_split_q<MODE, 2>(s, a, st, nb);
+        case 4: return launch_cfust_split_q<MODE, 4>(s, a, st, nb);
+        case 8: return launch_cfust_split_q<MODE, 8>(s, a, st, nb);
+        default: return int(cudaErrorInvalidValue);
+    }
 }
 
 template <int MODE>
@@ -1617,6 +1689,10 @@ static int launch_cfust_mode(const DevState &s, EArgs &a, cudaStream_t st, int *
                 default: return int(cudaErrorInvalidValue);
             }
         }
+    }
+    if constexpr (MODE != 2) {   // statistics and density passes split alike: identical l bits
+        const int sp = split_factor(s);
+        if (sp > 1) return launch_cfust_split<MODE>(s, a, st, nb, sp);
     }
     switch (s.q) {
         case 1: return launch_cfust_q<1, MODE>(s, a, st, nb);

@@ -33,5 +33,5 @@ for _ in range(a.reps):
     ll = em.estep()
 ms, cnt = em.timing()
 print(f"lib={os.path.basename(cf._native.LIB_PATH)} cfg{a.config} n={a.n} slice={a.full_slice} "
-      f"em_iters={a.em_iters} loglik={ll:.6f} estep_ms={ms[0] / max(1, cnt[0]):.3f} "
+      f"em_iters={a.em_iters} loglik={ll:.6f} estep_ms={ms[0] / max(1, cnt[0]):.4f} "
       f"us_per_obs={1e3 * ms[0] / max(1, cnt[0]) / a.n:.3f}")
