@@ -28,6 +28,7 @@ struct CompDev {
     double psi_half_m0;           // digamma(m0/2) for e1 - e2 (reading A5)
     double lgc_m0;                // lgamma((m0+1)/2) - lgamma(m0/2)      (t_1 density, df m0)
     double lgc_m0m1;              // lgamma(m0/2) - lgamma((m0-1)/2)      (t_1 density, df m0-1)
+    double lbt[3];                // log B(m/2, 1/2) at m = m0, m0+1, m0+2  (t_1 CDFs of T_1 terms)
     double inv_nu;                // 1 / nu
     double log_half_nu;           // log(nu / 2)
 };
@@ -77,21 +78,23 @@ __device__ inline double dev_trigamma(double x) {
 // Continued fraction of the regularized incomplete beta (modified Lentz):
 //   I_x(a,b) = x^a (1-x)^b / (a B(a,b)) * cf(a,b,x),  converging fast for x < (a+1)/(a+b+2).
 __device__ inline double dev_betacf(double a, double b, double x) {
+    // reciprocals by div_fast (rcp.approx + Newton, no IEEE slow-path call): |d|, |c| >= fpmin are
+    // normal numbers; the continued fraction needs no correctly rounded division
     const double fpmin = 1e-300;
     double c = 1.0;
     double d = 1.0 - (a + b) * x / (a + 1.0);
     d = (fabs(d) < fpmin) ? fpmin : d;
-    d = 1.0 / d;
+    d = div_fast(1.0, d);
     double h = d;
     for (int m = 1; m <= 4000; ++m) {
         const double m2 = 2.0 * m;
-        const double num_e = m * (b - m) * x / ((a + m2 - 1.0) * (a + m2));
-        d = 1.0 + num_e * d; d = (fabs(d) < fpmin) ? fpmin : d; d = 1.0 / d;
-        c = 1.0 + num_e / c; c = (fabs(c) < fpmin) ? fpmin : c;
+        const double num_e = m * (b - m) * x * div_fast(1.0, (a + m2 - 1.0) * (a + m2));
+        d = 1.0 + num_e * d; d = (fabs(d) < fpmin) ? fpmin : d; d = div_fast(1.0, d);
+        c = 1.0 + div_fast(num_e, c); c = (fabs(c) < fpmin) ? fpmin : c;
         h *= d * c;
-        const double num_o = -(a + m) * (a + b + m) * x / ((a + m2) * (a + m2 + 1.0));
-        d = 1.0 + num_o * d; d = (fabs(d) < fpmin) ? fpmin : d; d = 1.0 / d;
-        c = 1.0 + num_o / c; c = (fabs(c) < fpmin) ? fpmin : c;
+        const double num_o = -(a + m) * (a + b + m) * x * div_fast(1.0, (a + m2) * (a + m2 + 1.0));
+        d = 1.0 + num_o * d; d = (fabs(d) < fpmin) ? fpmin : d; d = div_fast(1.0, d);
+        c = 1.0 + div_fast(num_o, c); c = (fabs(c) < fpmin) ? fpmin : c;
         const double del = d * c;
         h *= del;
         if (fabs(del - 1.0) <= 1e-16) break;
@@ -99,13 +102,19 @@ __device__ inline double dev_betacf(double a, double b, double x) {
     return h;
 }
 
-// Univariate Student-t CDF with real df m:  P(T <= t) = 1 - I_{m/(m+t^2)}(m/2, 1/2)/2 for t >= 0.
-__device__ inline double dev_t_cdf(double t, double m) {
+// log B(m/2, 1/2), the t_1 CDF normaliser; the E-step takes it from CompDev::lbt (per component,
+// df m0, m0+1, m0+2) so the per-pair T_1 evaluations carry no lgamma.
+__device__ inline double dev_t_lbeta(double m) {
+    return lgamma(0.5 * m) + 0.5723649429247001 - lgamma(0.5 * m + 0.5);   // lgamma(1/2) = log(pi)/2
+}
+
+// Univariate Student-t CDF with real df m:  P(T <= t) = 1 - I_{m/(m+t^2)}(m/2, 1/2)/2 for t >= 0;
+// lbeta = log B(m/2, 1/2) (dev_t_lbeta).
+__device__ inline double dev_t_cdf(double t, double m, double lbeta) {
     if (isinf(t)) return t > 0 ? 1.0 : 0.0;
     const double t2 = t * t;
     const double x = m / (m + t2), xc = t2 / (m + t2);
     const double a = 0.5 * m, b = 0.5;
-    const double lbeta = lgamma(a) + lgamma(b) - lgamma(a + b);
     const double lx = (x > 0.5) ? log1p(-xc) : log(x);
     const double lxc = (xc > 0.5) ? log1p(-x) : log(xc);
     const double front = exp(a * lx + b * lxc - lbeta);
@@ -115,6 +124,7 @@ __device__ inline double dev_t_cdf(double t, double m) {
     if (!(xc > 0.0)) tail = 0.5;
     return (t >= 0.0) ? 1.0 - tail : tail;
 }
+__device__ inline double dev_t_cdf(double t, double m) { return dev_t_cdf(t, m, dev_t_lbeta(m)); }
 
 // log of the univariate t density t_1(0; loc, s2, m) given lgc = lgamma((m+1)/2) - lgamma(m/2).
 __device__ __forceinline__ double dev_t1_logpdf0(double loc, double s2, double m, double lgc) {

@@ -223,13 +223,13 @@ __device__ __forceinline__ double split_sum(double v) {
 // T_R(b; 0, S, m): R = 0 -> 1; R = 1 -> univariate t CDF; R >= 2 -> lattice rule with
 // univariate-prioritisation reordering (ascending b_k / sqrt(S_kk), stable; reading A13).
 template <int R, int NP, int SPLIT = 1>
-__device__ __noinline__ double T_eval(const double *b, const double *S, int lds, double m,
+__device__ __noinline__ double T_eval(const double *b, const double *S, int lds, double m, double lbt,
                                       const double *__restrict__ chi, const double *__restrict__ W, int M,
                                       int lane) {
     if constexpr (R == 0) {
         return 1.0;
     } else if constexpr (R == 1) {
-        return isinf(m) ? Phi(b[0] / sqrt(S[0])) : dev_t_cdf(b[0] / sqrt(S[0]), m);   // m = inf: normal family
+        return isinf(m) ? Phi(b[0] / sqrt(S[0])) : dev_t_cdf(b[0] / sqrt(S[0]), m, lbt);   // m = inf: normal family
     } else {
         double binv[R], Cn[R * (R - 1) / 2];
         if (!sov_setup<R>(b, S, lds, binv, Cn)) return CUDART_NAN;
@@ -395,7 +395,7 @@ __device__ void pair_eval_direct(const CompDev &cp, int p, const double *__restr
                                   log(rho), family, perm, acc);
     const double F = ok ? acc[0] : 0.0;
     double T0 = F / double(M);
-    if (Q == 1) T0 = T_eval<1, 1>(ws.b, cp.Lam, QMAX, nrm ? CUDART_INF : m0, chi, W, M, lane);   // exact T_1
+    if (Q == 1) T0 = T_eval<1, 1>(ws.b, cp.Lam, QMAX, nrm ? CUDART_INF : m0, cp.lbt[0], chi, W, M, lane);   // exact T_1
     const double e1me2_a5 = nrm ? 0.0 : cp.psi_half_m0 - log(0.5 * rho) - m0 / rho;
     if (!(T0 >= TMIN) || !(F > 0.0)) {   // reading A16
         res[0] = -CUDART_INF;
@@ -460,10 +460,10 @@ __device__ void pair_eval(const CompDev &cp, int p, const double *__restrict__ W
     if (MODE != 1 && e1_exact) {   // exact e1 = (sum f lv)/(sum f) - log rho on T0's points (R2')
         double wsum;
         const double T0lat = T_eval_w<Q, Tune<Q>::NP, SPLIT>(ws.b, cp.Lam, QMAX, chi, chi + CHI_LV * M, W, M, lane, &wsum);
-        T0 = (Q == 1) ? T_eval<1, 1>(ws.b, cp.Lam, QMAX, m0, chi, W, M, lane) : T0lat;   // density: exact T_1
+        T0 = (Q == 1) ? T_eval<1, 1>(ws.b, cp.Lam, QMAX, m0, cp.lbt[0], chi, W, M, lane) : T0lat;   // density: exact T_1
         e1x = wsum / T0lat - log(rho);
     } else {
-        T0 = T_eval<Q, Tune<Q>::NP, SPLIT>(ws.b, cp.Lam, QMAX, mT0, chi, W, M, lane);
+        T0 = T_eval<Q, Tune<Q>::NP, SPLIT>(ws.b, cp.Lam, QMAX, mT0, cp.lbt[0], chi, W, M, lane);
     }
     if (MODE == 1) {
         res[0] = (T0 >= TMIN) ? Q * CUDART_LN2 + logt + log(T0) : -CUDART_INF;
@@ -474,7 +474,7 @@ __device__ void pair_eval(const CompDev &cp, int p, const double *__restrict__ W
         const double sq2 = sqrt((m0 + 2.0) / rho);
 #pragma unroll
         for (int k = 0; k < Q; ++k) ws.b[k] = c[k] * sq2;
-        T2 = T_eval<Q, Tune<Q>::NP, SPLIT>(ws.b, cp.Lam, QMAX, m0 + 2.0, chi + CHI_M2 * M, W, M, lane);
+        T2 = T_eval<Q, Tune<Q>::NP, SPLIT>(ws.b, cp.Lam, QMAX, m0 + 2.0, cp.lbt[2], chi + CHI_M2 * M, W, M, lane);
     }
     res[1] = nrm ? 0.0 : cp.psi_half_m0 - log(0.5 * rho) - m0 / rho;      // e1 - e2, reading A5
     if (!(T0 >= TMIN)) {                                        // reading A16
@@ -535,7 +535,7 @@ __device__ void pair_eval(const CompDev &cp, int p, const double *__restrict__ W
                     }
                     ++ib;
                 }
-                const double val = T_eval<Q2, Tune<Q>::NP, SPLIT>(ws.bc, ws.Sc, QMAX, mT0, chi, W, M, lane);
+                const double val = T_eval<Q2, Tune<Q>::NP, SPLIT>(ws.bc, ws.Sc, QMAX, mT0, cp.lbt[0], chi, W, M, lane);
                 ws.Tkt[k * QMAX + t] = val;
                 ws.Tkt[t * QMAX + k] = val;            // symmetric in {k, t} (A17)
             }
@@ -546,7 +546,7 @@ __device__ void pair_eval(const CompDev &cp, int p, const double *__restrict__ W
     for (int k = 0; k < Q; ++k) {
         double tk = 1.0;
         if constexpr (Q >= 2)
-            tk = T_eval<Q1, Tune<Q>::NP, SPLIT>(ws.ct[k], ws.St[k], QMAX, nrm ? CUDART_INF : m0 + 1.0, chi + CHI_M1 * M, W, M, lane);
+            tk = T_eval<Q1, Tune<Q>::NP, SPLIT>(ws.ct[k], ws.St[k], QMAX, nrm ? CUDART_INF : m0 + 1.0, cp.lbt[1], chi + CHI_M1 * M, W, M, lane);
         ws.Tk[k] = tk;
         h[k] = ws.phi[k] * tk;
     }
@@ -1406,7 +1406,7 @@ __device__ int mstep_warp(const DevState &s, int i, MsWork &w, int lane) {
 struct DvWork {
     double Sg[PMAX * PMAX], D[PMAX * QMAX], Om[PMAX * PMAX], Lc[PMAX * PMAX];
     CompDev cd;
-    double lg[5];
+    double lg[8];
     int ok;
 };
 
@@ -1437,12 +1437,13 @@ __device__ int derive_warp(const DevState &s, int i, DvWork &w, CompDev &cd_out,
         for (int a = 0; a < p; ++a) cd.A[k * PMAX + a] = x[a];
     }
     const double nu = s.nu[i], m0 = nu + p;
-    if (lane < 5) {   // the transcendental constants in parallel
+    if (lane < 8) {   // the transcendental constants in parallel
         double v = 0.0;
         if (lane == 0) v = lgamma(0.5 * m0) - lgamma(0.5 * nu);
         else if (lane == 1) v = lgamma(0.5 * (m0 + 1.0)) - lgamma(0.5 * m0);
         else if (lane == 2) v = lgamma(0.5 * m0) - lgamma(0.5 * (m0 - 1.0));
         else if (lane == 3) v = dev_digamma(0.5 * m0);
+        else if (lane >= 5) v = dev_t_lbeta(m0 + double(lane - 5));   // log B(m/2, 1/2), m = m0, m0+1, m0+2
         else
             for (int a = 0; a < p; ++a) v += 2.0 * log(cd.L[a * PMAX + a]);
         w.lg[lane] = v;
@@ -1475,6 +1476,7 @@ __device__ int derive_warp(const DevState &s, int i, DvWork &w, CompDev &cd_out,
         cd.psi_half_m0 = w.lg[3];
         cd.lgc_m0 = w.lg[1];
         cd.lgc_m0m1 = w.lg[2];
+        for (int k = 0; k < 3; ++k) cd.lbt[k] = w.lg[5 + k];
         cd.inv_nu = 1.0 / nu;
         cd.log_half_nu = log(0.5 * nu);
     }
