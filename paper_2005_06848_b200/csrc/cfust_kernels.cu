@@ -139,8 +139,7 @@ __device__ __forceinline__ double sov_lane_sum(const double (&binv)[R], const do
             for (int j = 0; j < NPTS; ++j) {
                 const double w = __ldg(W + k * M + l0 + 32 * j);   // lattice coordinate k (table)
                 double u = w * e[j];
-                u = (u < UMIN) ? UMIN : u;   // clamps (reading A15); plain compares, no NaN semantics
-                u = (u > UMAX) ? UMAX : u;
+                u = clamp_u(u, UMIN, UMAX);   // clamps (reading A15)
                 z[j][k - 1] = Phiinv(u);
                 double a = s[j] * binv[k];
 #pragma unroll
@@ -326,8 +325,7 @@ __device__ __noinline__ bool sov_direct(const double *b, const double *S, int ld
                 f *= e;
             }
             double u = __ldg(W + (k + 1) * M + l) * e;
-            u = (u < UMIN) ? UMIN : u;
-            u = (u > UMAX) ? UMAX : u;
+            u = clamp_u(u, UMIN, UMAX);
             xi[k] = Phiinv(u);
         }
         const double w = sn ? 1.0 : m0r * s * s;

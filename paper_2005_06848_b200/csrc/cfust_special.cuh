@@ -62,6 +62,10 @@ __device__ __forceinline__ double div_fast(double p, double q) {
 #define CFUST_OWN_ELEM 1   // own branch-free exp/log/sqrt; with the seeded Phi^{-1} 11% faster E-step
 #endif                     // than libdevice (profiles/r01_seed_variants.log)
 
+#ifndef CFUST_INTSEL
+#define CFUST_INTSEL 0   // 1: sign / range tests on the integer image of the double (INT pipe, not DSETP)
+#endif
+
 #ifndef CFUST_EXP_TAB
 #define CFUST_EXP_TAB 0
 #endif
@@ -113,7 +117,13 @@ __device__ __forceinline__ double exp_neg(double x) {
     const double r = fma(kd, -2.3190468138462996e-17, fma(kd, -0.69314718055994528623, x));
     const double p = horner_c(c_EXPC, r);
     const double res = __hiloint2double(__double2hiint(p) + k * (1 << 20), __double2loint(p));
+#if CFUST_INTSEL
+    // x < -708 <=> negative with |x| > 708: unsigned high word above that of -708 (0xC0862000); the
+    // few doubles in (-708 - 2^-43, -708) pass through and get their (normal, accurate) value
+    return (unsigned(__double2hiint(x)) > 0xC0862000u) ? 0.0 : res;
+#else
     return (x < -708.0) ? 0.0 : res;
+#endif
 #else
     return exp(x);
 #endif
@@ -177,7 +187,11 @@ __device__ __forceinline__ double Phi_fast(double x) {
     const double x4 = hi * hi, x8 = x4 * x4;
     const double t = e * div_fast(estrin_c(c_PH_P, ax, hi, x4, x8), estrin_c(c_PH_Q, ax, hi, x4, x8));
 #endif
+#if CFUST_INTSEL
+    return (__double2hiint(x) < 0) ? t : 1.0 - t;   // sign bit (x = -0: t = 1/2 either way)
+#else
     return (x < 0.0) ? t : 1.0 - t;
+#endif
 }
 
 // Phi^{-1}(u), 0 < u < 1.  1 - u is exact for u >= 1/2; 2t is exact; log(2t) is accurate to
@@ -265,7 +279,26 @@ __device__ __forceinline__ double Phiinv_seed(double u) {
     const double R = div_fast(horner_c(c_PH_P, ax), horner_c(c_PH_Q, ax));
     const double r = 2.5066282746310002 * fma(t, ep, -R);
     const double x = fma(r, fma(r, fma(r, (2.0 * hi + 1.0) * (1.0 / 6.0), -0.5 * ax), 1.0), -ax);
+#if CFUST_INTSEL
+    return (__double2hiint(u) < 0x3FE00000) ? x : -x;   // u in (0, 1): u < 1/2 <=> high word below 0.5's
+#else
     return (u < 0.5) ? x : -x;
+#endif
+}
+
+// u clamped to [UMIN, UMAX] for u >= 0 (u = w e with w, e in [0, 1]); with CFUST_INTSEL on the
+// integer image (non-negative doubles order like their bit patterns).
+__device__ __forceinline__ double clamp_u(double u, double lo, double hi) {
+#if CFUST_INTSEL
+    long long b = __double_as_longlong(u);
+    const long long bl = __double_as_longlong(lo), bh = __double_as_longlong(hi);
+    b = (b < bl) ? bl : b;
+    b = (b > bh) ? bh : b;
+    return __longlong_as_double(b);
+#else
+    u = (u < lo) ? lo : u;   // plain compares, no NaN semantics
+    return (u > hi) ? hi : u;
+#endif
 }
 
 #ifndef CFUST_PHIINV_SEED
