@@ -38,7 +38,11 @@ extern "C" {
 #define CFUST_EUNDERFLOW -5  /* all g component densities are 0 at some y_j   */
 #define CFUST_EEMPTY -6      /* S0_i < 1e-10: empty component in the M-step    */
 #define CFUST_ECUDA -7       /* CUDA runtime error / no device                               */
-#define CFUST_ENCCL -8       /* NCCL error                                                   */
+#define CFUST_ENCCL -8       /* NCCL error: a failed collective, an NCCL asynchronous error seen
+                                while waiting (ncclCommGetAsyncError is polled), or a wait longer
+                                than the environment's CFUST_NCCL_TIMEOUT_S seconds (if set).  The
+                                communicator is then aborted and every later call on the context
+                                returns CFUST_ENCCL (fail fast; no elastic recovery).           */
 
 typedef struct cfust_ctx cfust_ctx;   /* opaque */
 

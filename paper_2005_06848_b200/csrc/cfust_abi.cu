@@ -19,6 +19,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <string>
+#include <thread>
 #include <vector>
 
 using namespace cfust;
@@ -32,6 +33,7 @@ struct cfust_ctx {
     double *h_pin = nullptr;       // pinned: [0] loglik, [1..] stats staging
     int *h_status = nullptr;       // pinned [4]
     ncclComm_t comm = nullptr;
+    bool comm_failed = false;      // an NCCL error or timeout aborted the communicator: every call fails
     int world = 1, rank = 0;
     bool have_stats = false;
     bool timing = false;
@@ -149,9 +151,44 @@ int check_status(cfust_ctx *ctx) {
     return CFUST_OK;
 }
 
+// Wait for the context stream.  With a communicator the wait polls (cudaStreamQuery) and checks
+// ncclCommGetAsyncError, and optionally a deadline, so that a failed or vanished peer turns into
+// CFUST_ENCCL on this rank (communicator aborted) instead of a hang — fail fast, SURVEY §5.
+int wait_stream(cfust_ctx *ctx) {
+    if (ctx->comm_failed) return fail(ctx, CFUST_ENCCL, "communicator aborted by an earlier NCCL failure");
+    if (!ctx->comm) {
+        CU(cudaStreamSynchronize(ctx->stream));
+        return CFUST_OK;
+    }
+    const char *to = std::getenv("CFUST_NCCL_TIMEOUT_S");   // read per wait: settable at any time
+    const double timeout_s = to ? std::atof(to) : 0.0;
+    const auto t0 = std::chrono::steady_clock::now();
+    for (;;) {
+        const cudaError_t q = cudaStreamQuery(ctx->stream);
+        if (q == cudaSuccess) return CFUST_OK;
+        if (q != cudaErrorNotReady) return fail(ctx, CFUST_ECUDA, cudaGetErrorString(q));
+        ncclResult_t ae = ncclSuccess;
+        const ncclResult_t r = ncclCommGetAsyncError(ctx->comm, &ae);
+        std::string why;
+        if (r != ncclSuccess || ae != ncclSuccess)
+            why = std::string("NCCL async error: ") + ncclGetErrorString(r != ncclSuccess ? r : ae);
+        else if (timeout_s > 0.0 &&
+                 std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count() > timeout_s)
+            why = "collective wait exceeded CFUST_NCCL_TIMEOUT_S";
+        if (!why.empty()) {
+            ncclCommAbort(ctx->comm);
+            ctx->comm = nullptr;
+            ctx->comm_failed = true;
+            return fail(ctx, CFUST_ENCCL, why);
+        }
+        std::this_thread::yield();
+    }
+}
+
 int fetch_status_and_sync(cfust_ctx *ctx) {
     CU(cudaMemcpyAsync(ctx->h_status, ctx->s.status, sizeof(int) * 4, cudaMemcpyDeviceToHost, ctx->stream));
-    CU(cudaStreamSynchronize(ctx->stream));
+    const int rc = wait_stream(ctx);
+    if (rc) return rc;
     return check_status(ctx);
 }
 
@@ -169,6 +206,7 @@ void acc_phase(cfust_ctx *ctx, int a, int b, int slot) {
 }
 
 int reset_status(cfust_ctx *ctx) {
+    if (ctx->comm_failed) return fail(ctx, CFUST_ENCCL, "communicator aborted by an earlier NCCL failure");
     CU(cudaMemsetAsync(ctx->s.status, 0, sizeof(int) * 4, ctx->stream));
     return CFUST_OK;
 }
@@ -692,10 +730,7 @@ int ensure_init_ws(cfust_ctx *ctx, int m) {
     return CFUST_OK;
 }
 
-int sync_ctx(cfust_ctx *ctx) {
-    CU(cudaStreamSynchronize(ctx->stream));
-    return CFUST_OK;
-}
+int sync_ctx(cfust_ctx *ctx) { return wait_stream(ctx); }
 
 int allreduce_sum(cfust_ctx *ctx, double *buf, size_t len) {
     if (ctx->comm) NC(ncclAllReduce(buf, buf, len, ncclDouble, ncclSum, ctx->comm, ctx->stream));

@@ -44,3 +44,23 @@ def test_one_rank_nccl_equals_no_nccl(cf, cfg_id, n):
     assert np.array_equal(la_, lb_) and np.array_equal(ta, tb) and lla == llb
     a.close()
     b.close()
+
+
+def test_collective_wait_timeout_fails_fast(cf, monkeypatch):
+    """Failure detection: with CFUST_NCCL_TIMEOUT_S below one E-step's duration the NCCL-aware wait
+    aborts the communicator and returns CFUST_ENCCL; every later call on the context fails the
+    same way (no silent fallback to single-rank semantics)."""
+    cfg = synth.with_n(synth.CONFIGS[2], 2000)
+    y, init, _ = synth.make_problem(cfg)
+    em = cf.CfustEM(y, cfg.g, cfg.q, init, synth.lattice_inputs(cfg), world=1, rank=0,
+                    nccl_id=cf.nccl_unique_id())
+    em.estep()                                        # healthy first
+    monkeypatch.setenv("CFUST_NCCL_TIMEOUT_S", "1e-9")   # read at every collective wait
+    with pytest.raises(cf.CfustError) as e:
+        em.estep()
+    assert e.value.code == cf.CFUST_ENCCL
+    monkeypatch.delenv("CFUST_NCCL_TIMEOUT_S")
+    with pytest.raises(cf.CfustError) as e2:
+        em.loglik()
+    assert e2.value.code == cf.CFUST_ENCCL
+    em.close()
