@@ -4,7 +4,7 @@
 // libdevice's normcdfinv is ~600 SASS instructions with several branches; inlined at every SOV
 // step it thrashed the instruction cache (ncu: stall "no_instruction" 8.1 per issue,
 // profiles/r01_*).  These are single rational approximations fitted by scripts/fit_special.py
-// (relative error <= 1.3e-15 in double evaluation; coefficients in cfust_coeffs.h, all positive
+// (relative error <= 1.3e-15 in double evaluation; Mills ratio (9,10); coefficients in cfust_coeffs.h, all positive
 // so Horner has no cancellation), one formula over the whole range so a warp never diverges:
 //   Phi(x):       t = exp(-x^2/2) R(|x|),  Phi = t (x < 0) or 1 - t (x >= 0)
 //   Phi^{-1}(u):  t = min(u, 1-u), FP32 seed z0 ~ -w U(sqrt(w)) (w = -log(2t)), then one
@@ -95,7 +95,8 @@ __device__ const double g_EXP2J[64] = {
 
 // exp(x) for x <= 709 (x >= -708 exact to ~1 ulp; below: 0, i.e. results < 1e-307 flush).
 // Default: x = k ln2 + r, |r| <= ln2/2: k from the 1.5*2^52 rounding trick, r with a two-part
-// ln2, Taylor to r^13, 2^k by adding k to the exponent field.
+// ln2, near-minimax degree-11 polynomial (c_EXPC, scripts/fit_special.py), 2^k by adding k to the
+// exponent field.
 // CFUST_EXP_TAB: x = (64 m + j) ln2/64 + r, |r| <= ln2/128: exp = 2^m 2^(j/64) (1 + q(r)),
 // q = r + ... + r^5/120 (truncation r^6/720 < 4e-17), 2^(j/64) from a 64-entry table:
 // 10 FP64 operations instead of 17.
