@@ -46,14 +46,20 @@ __device__ __forceinline__ double estrin_c(const double (&c)[N], double x, doubl
     else return fma(p3[1], x8, p3[0]);
 }
 
-// p / q for q > 0 normal: MUFU reciprocal seed + two Newton steps + one residual correction.
+#ifndef CFUST_DIV_NEWTON
+#define CFUST_DIV_NEWTON 1   // Newton steps on the reciprocal before the quotient correction
+#endif
+// p / q for normal q: MUFU reciprocal seed (relative error e0 ~ 2^-22), CFUST_DIV_NEWTON Newton
+// steps on 1/q (one: e0^2 ~ 1e-13), then the residual correction y + r (p - q y), itself a Newton
+// step on the quotient: error ~ e1^2 + rounding, i.e. within an ulp (tests/test_gpu_special.py).
 __device__ __forceinline__ double div_fast(double p, double q) {
     double r;
     asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(q));
-    double e = fma(-q, r, 1.0);
-    r = fma(r, e, r);
-    e = fma(-q, r, 1.0);
-    r = fma(r, e, r);
+#pragma unroll
+    for (int k = 0; k < CFUST_DIV_NEWTON; ++k) {
+        const double e = fma(-q, r, 1.0);
+        r = fma(r, e, r);
+    }
     const double y = p * r;
     return fma(fma(-q, y, p), r, y);
 }
@@ -279,7 +285,7 @@ __device__ __forceinline__ double Phiinv_seed(double u) {
     const double ep = exp_neg(0.5 * hi) * (1.0 + 0.5 * lo);                 // e^{z0^2/2} (exp_neg is valid to +709)
     const double R = div_fast(horner_c(c_PH_P, ax), horner_c(c_PH_Q, ax));
     const double r = 2.5066282746310002 * fma(t, ep, -R);
-    const double x = fma(r, fma(r, fma(r, (2.0 * hi + 1.0) * (1.0 / 6.0), -0.5 * ax), 1.0), -ax);
+    const double x = fma(r, fma(r, fma(r, fma(hi, 1.0 / 3.0, 1.0 / 6.0), -0.5 * ax), 1.0), -ax);
 #if CFUST_INTSEL
     return (__double2hiint(u) < 0x3FE00000) ? x : -x;   // u in (0, 1): u < 1/2 <=> high word below 0.5's
 #else
