@@ -136,6 +136,22 @@ __device__ __forceinline__ double exp_neg(double x) {
 #endif
 }
 
+// exp(xh + xl) for |xl| << 1 ulp-scale of xh (the low part of an exact square): xl joins the reduced
+// argument r, where it is representable, instead of a separate (1 + xl) factor (one op fewer).
+__device__ __forceinline__ double exp_neg2(double xh, double xl) {
+#if CFUST_OWN_ELEM && !CFUST_EXP_TAB
+    const double t = fma(xh, 1.4426950408889634074, 6755399441055744.0);
+    const int k = __double2loint(t);
+    const double kd = t - 6755399441055744.0;
+    const double r = fma(kd, -2.3190468138462996e-17, fma(kd, -0.69314718055994528623, xh)) + xl;
+    const double p = horner_c(c_EXPC, r);
+    const double res = __hiloint2double(__double2hiint(p) + k * (1 << 20), __double2loint(p));
+    return (xh < -708.0) ? 0.0 : res;
+#else
+    return exp_neg(xh) * (1.0 + xl);
+#endif
+}
+
 // log(x) for normal x > 0: x = m 2^e, m in [sqrt(1/2), sqrt(2)); log m = 2 atanh(s),
 // s = (m-1)/(m+1) (m-1 exact), series to s^21.  Relative accuracy holds as x -> 1 (e = 0).
 __device__ __forceinline__ double log_unit(double x) {
@@ -187,7 +203,7 @@ __device__ __forceinline__ double Phi_fast(double x) {
     const double ax = (fx < 40.0) ? fx : 40.0;   // exp(-800) = 0: Phi is exactly 0 or 1 beyond
     const double hi = ax * ax;
     const double lo = fma(ax, ax, -hi);
-    const double e = exp_neg(-0.5 * hi) * (1.0 - 0.5 * lo);
+    const double e = exp_neg2(-0.5 * hi, -0.5 * lo);
 #if CFUST_HORNER
     const double t = e * div_fast(horner_c(c_PH_P, ax), horner_c(c_PH_Q, ax));
 #else
@@ -282,7 +298,7 @@ __device__ __forceinline__ double Phiinv_seed(double u) {
     const double ax = fmin(double(w * seed_U32(v)), 37.5);                   // |z0|
     const double hi = ax * ax;
     const double lo = fma(ax, ax, -hi);
-    const double ep = exp_neg(0.5 * hi) * (1.0 + 0.5 * lo);                 // e^{z0^2/2} (exp_neg is valid to +709)
+    const double ep = exp_neg2(0.5 * hi, 0.5 * lo);                         // e^{z0^2/2} (valid to +709)
     const double R = div_fast(horner_c(c_PH_P, ax), horner_c(c_PH_Q, ax));
     const double r = 2.5066282746310002 * fma(t, ep, -R);
     const double x = fma(r, fma(r, fma(r, fma(hi, 1.0 / 3.0, 1.0 / 6.0), -0.5 * ax), 1.0), -ax);
