@@ -1655,6 +1655,9 @@ static int split_factor(const DevState &s) {
 
 template <int MODE, int SPLIT>
 static int launch_cfust_split_q(const DevState &s, EArgs &a, cudaStream_t st, int *nb) {
+    if constexpr (EW % SPLIT != 0) {   // experiment builds with small blocks (CFUST_EW < SPLIT)
+        return launch_cfust_split_q<MODE, SPLIT / 2>(s, a, st, nb);
+    } else {
     switch (s.q) {
         case 1: return launch_cfust_q<1, MODE, false, SPLIT>(s, a, st, nb);
         case 2: return launch_cfust_q<2, MODE, false, SPLIT>(s, a, st, nb);
@@ -1663,6 +1666,7 @@ static int launch_cfust_split_q(const DevState &s, EArgs &a, cudaStream_t st, in
         case 5: return launch_cfust_q<5, MODE, false, SPLIT>(s, a, st, nb);
         case 6: return launch_cfust_q<6, MODE, false, SPLIT>(s, a, st, nb);
         default: return int(cudaErrorInvalidValue);
+    }
     }
 }
 
