@@ -61,8 +61,9 @@ struct WarpScratch {
 // SOV point loop for T_R (chi-normal form, reading R-T): this lane's share of
 //   sum_l prod_k Phi(a_k(l)),  a_0 = s_l binv_0,  a_k = s_l binv_k - sum_{t<k} Cn_kt z_t,
 //   z_t = Phi^{-1}(clamp(w_{l,t+1} e_t)).
-// Per-q tuning of estep_cfust_kernel<Q> (measured on B200, profiles/r01_tuning.log; q = 3 re-tuned
-// to NP = 2 after the special-function refits, profiles/r01_retune.log):
+// Per-q tuning of estep_cfust_kernel<Q> (measured on B200, profiles/r01_tuning.log; re-checked after
+// the special-function refits, profiles/r01_retune.log: q = 3 with NP = 2 is 2.7 % faster on n = 3e5
+// slices but 16 % slower at the full cfg5 size, so NP = 1 stays):
 //   NP   lattice points per lane per loop iteration (independent SOV chains for the FP64 pipe),
 //   MB   resident blocks per SM the register budget must allow (__launch_bounds__).
 // CFUST_NP_Q<q> / CFUST_MB_Q<q> override them for experiment builds (scripts/build_variants.py).
@@ -73,7 +74,7 @@ struct WarpScratch {
 #define CFUST_NP_Q2 1
 #endif
 #ifndef CFUST_NP_Q3
-#define CFUST_NP_Q3 2
+#define CFUST_NP_Q3 1
 #endif
 #ifndef CFUST_NP_Q4
 #define CFUST_NP_Q4 2
