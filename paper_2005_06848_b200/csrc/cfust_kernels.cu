@@ -1292,7 +1292,9 @@ __device__ bool warp_chol(int n, const double *A, int lda, double *L, int ldl, i
     return true;
 }
 
+constexpr int KMAX = 2 + PMAX + PMAX * (PMAX + 1) / 2 + QMAX + QMAX * (QMAX + 1) / 2 + PMAX * QMAX + 1;
 struct MsWork {
+    double Sv[KMAX];   // this component's K statistics, staged from global memory in one coalesced read
     double S3[PMAX * PMAX], S5[QMAX * QMAX], mu[PMAX], D[PMAX * QMAX], B[PMAX * QMAX], Sg[PMAX * PMAX];
     double L5[QMAX * QMAX], Lt[PMAX * PMAX];
     double md;
@@ -1301,7 +1303,9 @@ struct MsWork {
 
 __device__ int mstep_warp(const DevState &s, int i, MsWork &w, int lane) {
     const int p = s.p, q = s.q, K = s.K;
-    const double *S = s.stats + size_t(i) * K;
+    for (int e = lane; e < K; e += 32) w.Sv[e] = s.stats[size_t(i) * K + e];
+    __syncwarp();
+    const double *S = w.Sv;
     const double S0 = S[0], S1 = S[1];
     const double *S2 = S + 2, *S3p = S2 + p, *S4 = S3p + p * (p + 1) / 2, *S5p = S4 + q;
     const double *S6 = S5p + q * (q + 1) / 2;
@@ -1427,7 +1431,15 @@ __device__ int derive_warp(const DevState &s, int i, DvWork &w, CompDev &cd_out,
         w.Om[a * PMAX + b] = v;
     }
     __syncwarp();
-    if (!warp_chol(p, w.Om, PMAX, cd.L, PMAX, lane, &w.ok)) return -4;
+    if (q == 0) {   // Omega = Sigma: its factor is the one just computed (bit-identical; no second chol)
+        for (int t = lane; t < PMAX * PMAX; t += 32) {
+            const int a = t / PMAX, b = t % PMAX;
+            cd.L[t] = (a < p && b <= a) ? w.Lc[t] : 0.0;
+        }
+        __syncwarp();
+    } else if (!warp_chol(p, w.Om, PMAX, cd.L, PMAX, lane, &w.ok)) {
+        return -4;
+    }
     for (int a = lane; a < PMAX; a += 32) cd.Linv[a] = (a < p) ? 1.0 / cd.L[a * PMAX + a] : 0.0;
     for (int a = lane; a < p; a += 32) cd.mu[a] = s.mu[size_t(i) * p + a];
     for (int k = lane; k < q; k += 32) {   // A = Delta' Omega^{-1}: one column of Omega^{-1} Delta per lane
