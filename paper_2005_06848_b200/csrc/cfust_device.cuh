@@ -138,10 +138,12 @@ __device__ __forceinline__ double dev_n1_logpdf0(double loc, double s2) {
 
 // Regularized incomplete gamma: series for P (x < a + 1), Legendre CF for Q otherwise.
 __device__ inline double dev_gamma_series_P(double a, double x, double lga) {
-    double sum = 1.0 / a, term = sum, ap = a;
+    // branch-free reciprocals (div_fast): x/(a+k) does not depend on the running term, so successive
+    // steps overlap instead of serialising on IEEE division's slow-path test
+    double sum = div_fast(1.0, a), term = sum, ap = a;
     for (int k = 0; k < 10000; ++k) {
         ap += 1.0;
-        term *= x / ap;
+        term *= div_fast(x, ap);
         sum += term;
         if (fabs(term) <= fabs(sum) * 1e-17) break;
     }
@@ -149,13 +151,13 @@ __device__ inline double dev_gamma_series_P(double a, double x, double lga) {
 }
 __device__ inline double dev_gamma_cf_Q(double a, double x, double lga) {
     const double fpmin = 1e-300;
-    double b = x + 1.0 - a, c = 1.0 / fpmin, d = 1.0 / b, h = d;
+    double b = x + 1.0 - a, c = 1.0 / fpmin, d = div_fast(1.0, b), h = d;
     for (int k = 1; k < 10000; ++k) {
         const double an = -k * (k - a);
         b += 2.0;
         d = an * d + b; d = (fabs(d) < fpmin) ? fpmin : d;
-        c = b + an / c; c = (fabs(c) < fpmin) ? fpmin : c;
-        d = 1.0 / d;
+        c = b + div_fast(an, c); c = (fabs(c) < fpmin) ? fpmin : c;
+        d = div_fast(1.0, d);
         const double del = d * c;
         h *= del;
         if (fabs(del - 1.0) <= 1e-16) break;
