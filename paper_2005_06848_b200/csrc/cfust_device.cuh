@@ -60,9 +60,9 @@ __device__ __forceinline__ double Phiinv(double u) { return Phiinv_fast(u); }
 __device__ inline double dev_digamma(double x) {
     double num = 0.0, den = 1.0;
     while (x < 16.0) { num = fma(num, x, den); den *= x; x += 1.0; }   // num/den += 1/x
-    const double r = 1.0 / x, r2 = r * r;
+    const double r = div_fast(1.0, x), r2 = r * r;
     const double ser = r2 * (1.0 / 12 - r2 * (1.0 / 120 - r2 * (1.0 / 252 - r2 * (1.0 / 240 - r2 * (1.0 / 132)))));
-    return log(x) - 0.5 * r - ser - num / den;
+    return log(x) - 0.5 * r - ser - div_fast(num, den);
 }
 
 // trigamma psi'(x), x > 0: recurrence sum 1/(x+k)^2 to x >= 16, then the asymptotic series
@@ -70,9 +70,9 @@ __device__ inline double dev_digamma(double x) {
 __device__ inline double dev_trigamma(double x) {
     double num = 0.0, den = 1.0;
     while (x < 16.0) { const double x2 = x * x; num = fma(num, x2, den); den *= x2; x += 1.0; }   // num/den += 1/x^2
-    const double r = 1.0 / x, r2 = r * r;
+    const double r = div_fast(1.0, x), r2 = r * r;
     const double ser = r * (1.0 + r * (0.5 + r * (1.0 / 6 - r2 * (1.0 / 30 - r2 * (1.0 / 42 - r2 * (1.0 / 30 - r2 * (5.0 / 66)))))));
-    return num / den + ser;
+    return div_fast(num, den) + ser;
 }
 
 // Continued fraction of the regularized incomplete beta (modified Lentz):

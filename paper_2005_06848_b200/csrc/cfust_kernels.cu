@@ -1251,12 +1251,12 @@ __device__ inline void chol_solve_dev(int n, const double *L, int ldl, double *x
     for (int i = 0; i < n; ++i) {
         double s = x[i];
         for (int k = 0; k < i; ++k) s -= L[i * ldl + k] * x[k];
-        x[i] = s / L[i * ldl + i];
+        x[i] = div_fast(s, L[i * ldl + i]);
     }
     for (int i = n - 1; i >= 0; --i) {
         double s = x[i];
         for (int k = i + 1; k < n; ++k) s -= L[k * ldl + i] * x[k];
-        x[i] = s / L[i * ldl + i];
+        x[i] = div_fast(s, L[i * ldl + i]);
     }
 }
 
@@ -1278,14 +1278,14 @@ __device__ bool warp_chol(int n, const double *A, int lda, double *L, int ldl, i
             double d = A[j * lda + j];
             for (int k = 0; k < j; ++k) d -= L[j * ldl + k] * L[j * ldl + k];
             *okflag = (d > 1e-300);
-            L[j * ldl + j] = *okflag ? sqrt(d) : 0.0;
+            L[j * ldl + j] = *okflag ? sqrt_fast(d) : 0.0;   // rsqrt + Newton: no IEEE slow path
         }
         __syncwarp();
         if (!*okflag) return false;
         for (int i = j + 1 + lane; i < n; i += 32) {
             double v = A[i * lda + j];
             for (int k = 0; k < j; ++k) v -= L[i * ldl + k] * L[j * ldl + k];
-            L[i * ldl + j] = v / L[j * ldl + j];
+            L[i * ldl + j] = div_fast(v, L[j * ldl + j]);
         }
         __syncwarp();
     }
@@ -1395,8 +1395,8 @@ __device__ int mstep_warp(const DevState &s, int i, MsWork &w, int lane) {
         for (int it = 0; it < 200; ++it) {
             const double gv = nu_equation(nu, cst);
             if (gv > 0.0) lo = nu; else hi = nu;
-            const double dg = 1.0 / nu - 0.5 * dev_trigamma(0.5 * nu);
-            double nn = nu - gv / dg;
+            const double dg = div_fast(1.0, nu) - 0.5 * dev_trigamma(0.5 * nu);
+            double nn = nu - div_fast(gv, dg);
             if (!(nn > lo && nn < hi)) nn = 0.5 * (lo + hi);
             const bool done = fabs(nn - nu) <= 1e-13 * nu || hi - lo <= 1e-13 * nu;
             nu = nn;
