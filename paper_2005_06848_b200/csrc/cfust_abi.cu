@@ -255,7 +255,7 @@ int enqueue_mstep(cfust_ctx *ctx) {
     Nvtx r("cfust:mstep");
     CUI(launch_mstep(ctx->s, ctx->stream));
     CUI(launch_chi(ctx->s, ctx->stream));
-    ctx->launches += (ctx->s.M > 0) ? 3 : 2;   // M-step, pi + derive, chi nodes
+    ctx->launches += mstep_launches() + ((ctx->s.M > 0) ? 1 : 0);   // M-step (+ pi, derive), chi nodes
     rec(ctx, 4);
     return CFUST_OK;
 }

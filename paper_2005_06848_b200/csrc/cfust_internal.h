@@ -44,6 +44,7 @@ constexpr int CHI_M1 = 1, CHI_M2 = 2, CHI_LV = 3, CHI_ROWS = 4;
 int launch_estep(const DevState &s, int mode, const int64_t *idx, int64_t cnt, double *pair_out,
                  cudaStream_t st, int *nblocks_out);
 int launch_reduce(const DevState &s, int nblocks, int mode, double *out, cudaStream_t st);
+int mstep_launches();
 int launch_mstep(const DevState &s, cudaStream_t st);
 int launch_derive(const DevState &s, cudaStream_t st);
 int launch_chi(const DevState &s, cudaStream_t st);

@@ -1529,6 +1529,38 @@ __global__ void __launch_bounds__(32) mstep_derive_kernel(DevState s) {
     if (rc != 0 && lane == 0) atomicMin(s.status + 1, rc);
 }
 
+// The whole M-step in one launch: one block, warp i = component i.  Phase 1 the ECM updates
+// (mstep_warp); block barrier; if no component failed (status[1], which also carries earlier
+// errors of the iteration), phase 2 pi and the derived quantities (derive_warp) — the same two
+// steps as mstep_kernel + mstep_derive_kernel without the second launch.
+union MsDvWork {
+    MsWork ms;
+    DvWork dv;
+};
+__global__ void __launch_bounds__(32 * GMAX) mstep_fused_kernel(DevState s) {
+    __shared__ MsDvWork w[GMAX];
+    const int i = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (i < s.g) {
+        const int rc = mstep_warp(s, i, w[i].ms, lane);
+        if (rc != 0 && lane == 0) atomicMin(s.status + 1, rc);
+    }
+    __syncthreads();
+    if (i >= s.g || reinterpret_cast<volatile int *>(s.status)[1] < 0) return;
+    if (lane == 0) {
+        double tot = 0.0, mine = 0.0;
+        for (int c = 0; c < s.g; ++c) {
+            double v = s.stats[size_t(c) * s.K] / s.n_total;
+            v = (v < 1e-10) ? 1e-10 : v;
+            tot += v;
+            if (c == i) mine = v;
+        }
+        s.pi[i] = mine / tot;
+    }
+    __syncwarp();
+    const int rc = derive_warp(s, i, w[i].dv, s.comp[i], lane);
+    if (rc != 0 && lane == 0) atomicMin(s.status + 1, rc);
+}
+
 __global__ void __launch_bounds__(32) derive_kernel(DevState s) {
     __shared__ DvWork w;
     const int i = blockIdx.x, lane = threadIdx.x;
@@ -1845,11 +1877,19 @@ int launch_reduce_cols(const double *partials, int nblocks, int stride, int ncol
     return int(cudaGetLastError());
 }
 
+#ifndef CFUST_MSTEP_FUSED
+#define CFUST_MSTEP_FUSED 1
+#endif
 int launch_mstep(const DevState &s, cudaStream_t st) {
+#if CFUST_MSTEP_FUSED
+    mstep_fused_kernel<<<1, 32 * s.g, 0, st>>>(s);
+#else
     mstep_kernel<<<s.g, 32, 0, st>>>(s);
     mstep_derive_kernel<<<s.g, 32, 0, st>>>(s);
+#endif
     return int(cudaGetLastError());
 }
+int mstep_launches() { return CFUST_MSTEP_FUSED ? 1 : 2; }
 
 int launch_derive(const DevState &s, cudaStream_t st) {
     derive_kernel<<<s.g, 32, 0, st>>>(s);
