@@ -188,12 +188,9 @@ __device__ inline double dev_chi2_quantile(double w, double m) {
     // small-v regime: P ~ x^a / Gamma(a+1)
     const double s_small = (log(w) + lga + log(a)) / a;   // lgamma(a+1) = lgamma(a) + log(a)
     if (!upper && s_small < s) s = s_small;
-    double lo = -745.0, hi = fmax(0.0, log(a)) + 1.0;
-    for (int k = 0; k < 100; ++k) {   // make sure hi brackets from above
-        const double g = dev_log_gamma_PQ(a, exp(hi), upper, lga) - ltarget;
-        if (upper ? (g < 0.0) : (g > 0.0)) break;
-        hi += 1.0;
-    }
+    // a-priori bracket, no evaluation: at x = e^{-745} log P ~ -745 a (below any log w), and at
+    // x = a e^{40} log Q ~ -x (below any log(1 - w) >= log 2^-53), so the root s lies in (lo, hi)
+    double lo = -745.0, hi = fmax(0.0, log(a)) + 40.0;
     if (!(s > lo && s < hi)) s = 0.5 * (lo + hi);
     for (int it = 0; it < 300; ++it) {
         const double x = exp(s);
