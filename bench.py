@@ -38,7 +38,7 @@ UNIT = "(obs·component)/s"
 FP64_PEAK_NOMINAL_TFLOPS = 148 * 64 * 2 * 1.965e9 / 1e12
 # Executed FP64 flops of the E-step kernel per (obs, component) pair at cfg2, from the ncu
 # counters 2*dfma + dadd + dmul over one full-size cfg2 E-step launch (n=1e5, 300000 pairs):
-# profiles/r01m_ncu_estep_cfg2_full.txt.  Re-measured whenever the kernel changes
+# profiles/r01m_ncu_estep_cfg2_full.txt, re-confirmed in r01n.  Re-measured whenever the kernel changes
 # (1.1417e7 with the (10,11) Mills rational, Taylor-13 exp and two-Newton division, r01h).
 FP64_FLOPS_PER_PAIR = {2: 9.985e6}
 # dram__bytes_read.sum + dram__bytes_write.sum of the same launch: 3.631 MB + 0 B
