@@ -44,6 +44,10 @@ FP64_FLOPS_PER_PAIR = {2: 9.985e6}
 # dram__bytes_read.sum + dram__bytes_write.sum of the same launch: 3.631 MB + 0 B
 # (profiles/r01m_ncu_estep_cfg2_full.txt).  Algorithmic bytes: y = 3.2 MB (+ node tables).
 TRAFFIC_BYTES_PER_LAUNCH = {2: 3.631e6}
+# sm__pipe_fp64_cycles_active (pct of peak, elapsed) of the same launch: the FP64 pipe's busy share,
+# which also counts DMUL/DADD/DSETP issue (one flop or none each) — the utilisation view beside the
+# flop-rate fraction (profiles/r01n_ncu_estep_cfg2_full.txt).
+FP64_PIPE_ACTIVE_NCU = {2: 0.659}
 
 
 def env_rank():
@@ -285,7 +289,7 @@ def main():
     if fpp:
         ach = fpp * pairs_local / (est_ms * 1e-3) / 1e12
         roof.update({"achieved": ach, "frac": ach / FP64_PEAK_NOMINAL_TFLOPS,
-                     "flops_per_pair": fpp})
+                     "flops_per_pair": fpp, "fp64_pipe_active_ncu": FP64_PIPE_ACTIVE_NCU.get(args.config)})
     else:
         roof.update({"achieved": None, "frac": None})
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
