@@ -2,6 +2,8 @@
 ragged n, each family / estimator / e1 option, through the C ABI against the oracle (per-pair
 outputs and the statistics; tolerances as tests/test_gpu_parity.py).  Covers shapes the five
 BASELINE configs do not (p = 1, 5, 7; q = 5; q > p; g = 1, 6, 7)."""
+import os
+
 import numpy as np
 import pytest
 
@@ -23,10 +25,11 @@ def cf():
 
 
 def _cases():
-    rng = np.random.default_rng(20260)
+    # CFUST_FUZZ_N / CFUST_FUZZ_SEED widen the sweep for assurance runs (profiles/r01_fuzz_wide.log)
+    rng = np.random.default_rng(int(os.environ.get("CFUST_FUZZ_SEED", "20260")))
     out = []
     opts = [{}, {"e1_exact": True}, {"family": "sn"}, {"estimator": "direct"}]
-    for k in range(40):
+    for k in range(int(os.environ.get("CFUST_FUZZ_N", "40"))):
         p = int(rng.integers(1, 9))
         q = int(rng.integers(0, 7))
         g = int(rng.integers(1, 9))
