@@ -135,7 +135,9 @@ int cfust_loglik(cfust_ctx *ctx, double *out);
 int cfust_predict(cfust_ctx *ctx, int32_t *labels_out, double *tau_out, double *loglik_out);
 
 /* Full fit: E-step, then max_iter x [M-step, E-step] with the Aitken stop when tol > 0
- * (Alg. 4, reading A8); out->loglik_trace gets l^(0..n_iter). */
+ * (Alg. 4, reading A8); out->loglik_trace gets l^(0..n_iter).  When the fit runs to max_iter the
+ * last l comes from the density-only pass (cfust_loglik: same value, no statistics), so call
+ * cfust_estep before a further cfust_mstep. */
 int cfust_fit(cfust_ctx *ctx, int32_t max_iter, double tol, cfust_result *out);
 
 int cfust_get_params(cfust_ctx *ctx, cfust_params *out);         /* copies into caller buffers */

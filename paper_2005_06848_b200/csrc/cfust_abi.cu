@@ -592,7 +592,10 @@ int cfust_fit(cfust_ctx *ctx, int32_t max_iter, double tol, cfust_result *out) {
     for (int k = 1; k <= max_iter; ++k) {
         rc = cfust_mstep(ctx);
         if (rc) break;
-        rc = cfust_estep(ctx, &l, nullptr);   // E-step at Psi^(k) yields l^(k) (trace convention)
+        // E-step at Psi^(k) yields l^(k) (trace convention).  After the last M-step only l is
+        // needed: the density-only pass (T0 alone, bitwise the same l) instead of the statistics
+        // pass — one full E-step fewer per fit (17 % of a 5-iteration cfg4/cfg5 fit).
+        rc = (k == max_iter) ? cfust_loglik(ctx, &l) : cfust_estep(ctx, &l, nullptr);
         if (rc) break;
         tr.push_back(l);
         out->n_iter = k;
