@@ -21,6 +21,10 @@
  *    no lattice is used.  lattice_z / lattice_shift hold max(q, 1) entries (q + 1 with
  *    opts.estimator == 1).
  *  - There is no CPU fallback: without a CUDA device every call fails with CFUST_ECUDA.
+ *  - Environment (optional): CFUST_SPLIT = 1|2|4|8 forces the warps per observation of the
+ *    small-n E-step (read at cfust_em_init; default: chosen from n and the q-tuned occupancy);
+ *    CFUST_NCCL_TIMEOUT_S = seconds bounds every collective wait (see CFUST_ENCCL).
+ *  - Each call and E-/M-step phase is an NVTX range ("cfust_fit", "cfust:estep-kernel", ...).
  */
 #ifndef CFUST_H
 #define CFUST_H
