@@ -50,9 +50,16 @@ def load_bench(paths: list[str]) -> dict[int, float]:
             objs = obj if isinstance(obj, list) else [obj]
         except json.JSONDecodeError:
             objs = [json.loads(l) for l in txt.splitlines() if l.strip().startswith("{")]
-        for o in objs:
-            if isinstance(o, dict) and "n_gpus" in o and "ms_per_step" in o and o.get("impl") != "reference":
-                times[int(o["n_gpus"])] = float(o["ms_per_step"])
+        stack = list(objs)
+        while stack:   # bench lines anywhere in the structure (a list, or nested under other keys)
+            o = stack.pop()
+            if isinstance(o, dict):
+                if "n_gpus" in o and "ms_per_step" in o and o.get("impl") != "reference":
+                    times[int(o["n_gpus"])] = float(o["ms_per_step"])
+                else:
+                    stack.extend(o.values())
+            elif isinstance(o, list):
+                stack.extend(o)
     return times
 
 
