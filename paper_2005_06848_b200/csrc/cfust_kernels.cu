@@ -1301,7 +1301,33 @@ struct MsWork {
     int ok;
 };
 
-__device__ int mstep_warp(const DevState &s, int i, MsWork &w, int lane) {
+__device__ double nu_update(const DevState &s, int i, double S0, double S7) {
+    const double cst = S7 / S0;
+    // nu: root of g(nu) = log(nu/2) - psi(nu/2) + 1 + S7/S0 on [nu_lo, nu_hi] (reading A7; g decreasing,
+    // clamped when there is no sign change): safeguarded Newton from the previous nu, the bracket kept and
+    // bisection taken whenever a step leaves it, to |dnu| <= 1e-13 nu (the oracle bisects to 1e-12: both
+    // land within that tolerance of the root).
+    double nu;
+    if (nu_equation(s.nu_hi, cst) > 0.0) nu = s.nu_hi;
+    else if (nu_equation(s.nu_lo, cst) < 0.0) nu = s.nu_lo;
+    else {
+        double lo = s.nu_lo, hi = s.nu_hi;
+        nu = fmin(fmax(s.nu[i], lo), hi);
+        for (int it = 0; it < 200; ++it) {
+            const double gv = nu_equation(nu, cst);
+            if (gv > 0.0) lo = nu; else hi = nu;
+            const double dg = div_fast(1.0, nu) - 0.5 * dev_trigamma(0.5 * nu);
+            double nn = nu - div_fast(gv, dg);
+            if (!(nn > lo && nn < hi)) nn = 0.5 * (lo + hi);
+            const bool done = fabs(nn - nu) <= 1e-13 * nu || hi - lo <= 1e-13 * nu;
+            nu = nn;
+            if (done) break;
+        }
+    }
+    return nu;
+}
+
+__device__ int mstep_warp(const DevState &s, int i, MsWork &w, int lane, bool do_nu = true) {
     const int p = s.p, q = s.q, K = s.K;
     for (int e = lane; e < K; e += 32) w.Sv[e] = s.stats[size_t(i) * K + e];
     __syncwarp();
@@ -1380,30 +1406,8 @@ __device__ int mstep_warp(const DevState &s, int i, MsWork &w, int lane) {
     for (int a = lane; a < p; a += 32) s.mu[size_t(i) * p + a] = w.mu[a];
     for (int t = lane; t < p * p; t += 32) s.sigma[size_t(i) * p * p + t] = w.Sg[t];
     for (int t = lane; t < p * q; t += 32) s.delta[size_t(i) * p * q + t] = w.D[t];
-    if (s.family == 1 || lane != 0) return 0;   // skew-normal / Gaussian: no nu
-    const double cst = S7 / S0;
-    // nu: root of g(nu) = log(nu/2) - psi(nu/2) + 1 + S7/S0 on [nu_lo, nu_hi] (reading A7; g decreasing,
-    // clamped when there is no sign change): safeguarded Newton from the previous nu, the bracket kept and
-    // bisection taken whenever a step leaves it, to |dnu| <= 1e-13 nu (the oracle bisects to 1e-12: both
-    // land within that tolerance of the root).
-    double nu;
-    if (nu_equation(s.nu_hi, cst) > 0.0) nu = s.nu_hi;
-    else if (nu_equation(s.nu_lo, cst) < 0.0) nu = s.nu_lo;
-    else {
-        double lo = s.nu_lo, hi = s.nu_hi;
-        nu = fmin(fmax(s.nu[i], lo), hi);
-        for (int it = 0; it < 200; ++it) {
-            const double gv = nu_equation(nu, cst);
-            if (gv > 0.0) lo = nu; else hi = nu;
-            const double dg = div_fast(1.0, nu) - 0.5 * dev_trigamma(0.5 * nu);
-            double nn = nu - div_fast(gv, dg);
-            if (!(nn > lo && nn < hi)) nn = 0.5 * (lo + hi);
-            const bool done = fabs(nn - nu) <= 1e-13 * nu || hi - lo <= 1e-13 * nu;
-            nu = nn;
-            if (done) break;
-        }
-    }
-    s.nu[i] = nu;
+    if (s.family == 1 || lane != 0 || !do_nu) return 0;   // skew-normal / Gaussian: no nu
+    s.nu[i] = nu_update(s, i, S0, S7);
     return 0;
 }
 
@@ -1537,15 +1541,23 @@ union MsDvWork {
     MsWork ms;
     DvWork dv;
 };
-__global__ void __launch_bounds__(32 * GMAX) mstep_fused_kernel(DevState s) {
+__global__ void __launch_bounds__(64 * GMAX) mstep_fused_kernel(DevState s) {
     __shared__ MsDvWork w[GMAX];
+    __shared__ double nu_new[GMAX];
     const int i = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const bool tnu = s.family != 1;   // skew-t: nu solved by warp g + i, concurrently with warp i's updates
     if (i < s.g) {
-        const int rc = mstep_warp(s, i, w[i].ms, lane);
+        const int rc = mstep_warp(s, i, w[i].ms, lane, false);
         if (rc != 0 && lane == 0) atomicMin(s.status + 1, rc);
+    } else if (tnu && i < 2 * s.g && lane == 0) {
+        const int c = i - s.g;
+        const double S0 = s.stats[size_t(c) * s.K], S7 = s.stats[size_t(c) * s.K + s.K - 1];
+        if (S0 >= 1e-10) nu_new[c] = nu_update(s, c, S0, S7);   // (S0 < 1e-10: warp c reports -6)
     }
     __syncthreads();
     if (i >= s.g || reinterpret_cast<volatile int *>(s.status)[1] < 0) return;
+    if (tnu && lane == 0) s.nu[i] = nu_new[i];
+    __syncwarp();
     if (lane == 0) {
         double tot = 0.0, mine = 0.0;
         for (int c = 0; c < s.g; ++c) {
@@ -1882,7 +1894,7 @@ int launch_reduce_cols(const double *partials, int nblocks, int stride, int ncol
 #endif
 int launch_mstep(const DevState &s, cudaStream_t st) {
 #if CFUST_MSTEP_FUSED
-    mstep_fused_kernel<<<1, 32 * s.g, 0, st>>>(s);
+    mstep_fused_kernel<<<1, 64 * s.g, 0, st>>>(s);
 #else
     mstep_kernel<<<s.g, 32, 0, st>>>(s);
     mstep_derive_kernel<<<s.g, 32, 0, st>>>(s);
