@@ -81,14 +81,19 @@ def lib():
         L.orc_derive.argtypes = [_I, _I, _PD, _PD, _D, _PD, _PD, _PD, _PD, _PD]
         L.orc_pair.restype = _I
         L.orc_pair.argtypes = [_I, _I, _PD, _PD, _PD, _PD, _PD, _D, _D, C.POINTER(_Lattice),
-                               _PD, _PD, _PD, _PD, _PD, _PD]
+                               _PD, _PD, _PD, _PD, _PD, _PD, _PD]
         L.orc_estep.restype = _I
         L.orc_estep.argtypes = [_I64, _I, _I, _I, _PD, _PD, _PD, _PD, _PD, _PD, C.POINTER(_Lattice),
                                 _I, _I, _PD, _PD, _PD, _PD]
+        L.orc_estep_b.restype = _I
+        L.orc_estep_b.argtypes = [_I64, _I, _I, _I, _PD, _PD, _PD, _PD, _PD, _PD, C.POINTER(_Lattice),
+                                  _I, _I, _PD, _PD, _PD, _PD, _PD]
+        L.orc_set_tie_flip.restype = None
+        L.orc_set_tie_flip.argtypes = [_I]
         L.orc_mstep.restype = _I
         L.orc_mstep.argtypes = [_I, _I, _I, _D, _PD, _PD, _PD, _PD, _PD, _PD, _D, _D, _I]
         L.orc_pair_sn.restype = _I
-        L.orc_pair_sn.argtypes = [_I, _I, _PD, _PD, _PD, _PD, _PD, _D, C.POINTER(_Lattice), _PD, _PD, _PD]
+        L.orc_pair_sn.argtypes = [_I, _I, _PD, _PD, _PD, _PD, _PD, _D, C.POINTER(_Lattice), _PD, _PD, _PD, _PD]
         L.orc_aitken_stop.restype = _I
         L.orc_aitken_stop.argtypes = [_D, _D, _D, _D]
         L.orc_fit.restype = _I
@@ -218,13 +223,13 @@ def pair(y, mu, sigma, delta, nu, lat: Lattice | None, e1_exact: bool = False, f
     if family == "sn":
         ones = np.ones(lat.M if (lat is not None and q >= 2) else 1)
         rc = lib().orc_pair_sn(p, q, _p(y), _p(mu), _p(dv["L"]), _p(A), _p(Lam), float(dv["logdet"]),
-                               lat.ptr if lat is not None else None, _p(ones), _p(out), _p(gap))
+                               lat.ptr if lat is not None else None, _p(ones), _p(out), _p(gap), None)
         assert rc == OK, rc
         return {"logf": out[0], "e1me2": out[1], "e2": out[2], "e3": out[3:3 + q],
                 "e4": out[3 + q:].reshape(q, q), "gap": gap[0]}
     rc = lib().orc_pair(p, q, _p(y), _p(mu), _p(dv["L"]), _p(A), _p(Lam), float(nu), float(dv["kappa"]),
                         lat.ptr if lat is not None else None, _p(tabs[0]), _p(tabs[1]), _p(tabs[2]),
-                        _p(lv) if lv is not None else None, _p(out), _p(gap))
+                        _p(lv) if lv is not None else None, _p(out), _p(gap), None)
     assert rc == OK, rc
     return {"logf": out[0], "e1me2": out[1], "e2": out[2], "e3": out[3:3 + q],
             "e4": out[3 + q:].reshape(q, q), "gap": gap[0]}
@@ -237,9 +242,17 @@ def _params(params: dict, g: int, p: int, q: int):
             _f64(params["nu"]).reshape(g))
 
 
+def set_tie_flip(on: bool):
+    """Reading A14 harness: sort near-tied reordering keys (within 1e-12) in the opposite order."""
+    lib().orc_set_tie_flip(1 if on else 0)
+
+
 def estep(y, params: dict, q: int, lat: Lattice | None, nthreads=None, pairs=False, gaps=False,
-          e1_exact: bool = False, family: str = "st", estimator: str = "analytic"):
-    """Full E-step.  Returns dict(stats [g*K+1], loglik, pairs [n,g,4+q+q*q] optional)."""
+          e1_exact: bool = False, family: str = "st", estimator: str = "analytic", bounds=False,
+          tie_flip=False):
+    """Full E-step.  Returns dict(stats [g*K+1], loglik, pairs [n,g,4+q+q*q] optional,
+    gaps [n,g] (smallest reordering-key gap), bounds [n,g,q+q*q] (running error bounds of e3/e4,
+    analytic estimator)).  tie_flip: evaluate near-tied orders reversed (reading A14)."""
     y = _f64(y)
     n, p = y.shape
     g = len(params["pi"])
@@ -249,10 +262,21 @@ def estep(y, params: dict, q: int, lat: Lattice | None, nthreads=None, pairs=Fal
     ll = np.zeros(1)
     po = np.zeros((n, g, 4 + q + q * q)) if pairs else None
     gp = np.full((n, g), np.inf) if gaps else None
-    rc = lib().orc_estep(n, p, q, g, _p(y), _p(pi), _p(mu), _p(sg), _p(de), _p(nu),
-                         lat.ptr if lat is not None else None, _nt(nthreads), _flags(e1_exact, family, estimator),
-                         _p(po) if pairs else None, _p(stats), _p(ll), _p(gp) if gaps else None)
+    bd = np.zeros((n, g, max(q + q * q, 1))) if bounds else None
+    if tie_flip:
+        set_tie_flip(True)
+    try:
+        rc = lib().orc_estep_b(n, p, q, g, _p(y), _p(pi), _p(mu), _p(sg), _p(de), _p(nu),
+                               lat.ptr if lat is not None else None, _nt(nthreads),
+                               _flags(e1_exact, family, estimator),
+                               _p(po) if pairs else None, _p(stats), _p(ll), _p(gp) if gaps else None,
+                               _p(bd) if bounds else None)
+    finally:
+        if tie_flip:
+            set_tie_flip(False)
     out = {"rc": rc, "stats": stats, "loglik": ll[0]}
+    if bounds:
+        out["bounds"] = bd[..., :q + q * q]
     if pairs:
         out["pairs"] = po
     if gaps:

@@ -66,32 +66,57 @@ double orc_norm_quantile(double u) {
     return z;
 }
 
-/* Regularized incomplete gamma P(a,x): power series, valid for x < a+1. */
+/* Regularized incomplete gamma P(a,x) for x < a+1: the series of DLMF 8.7.1,
+ *   gamma*(a,x) x^a = e^{-x} x^a / Gamma(a+1) * sum_{k>=0} x^k / ((a+1)(a+2)...(a+k)),
+ * summed term by term until a term no longer changes the sum. */
 static double gamma_p_series(double a, double x) {
-    double term = 1.0 / a, sum = term;
-    for (int n = 1; n < 100000; ++n) {
-        term *= x / (a + n);
+    double sum = 0.0, term = 1.0;
+    for (int k = 0; k < 100000; ++k) {
+        const double before = sum;
         sum += term;
-        if (fabs(term) < fabs(sum) * 1e-17) break;
+        if (sum == before) break;
+        term = term * x / (a + k + 1.0);
     }
-    return sum * exp(-x + a * log(x) - lgamma(a));
+    return exp(a * log(x) - x - lgamma(a + 1.0)) * sum;
 }
 
-/* Regularized incomplete gamma Q(a,x): Legendre continued fraction (modified Lentz), x >= a+1. */
-static double gamma_q_cf(double a, double x) {
-    const double tiny = 1e-300;
-    double b = x + 1.0 - a, c = 1.0 / tiny, d = 1.0 / b, h = d;
-    for (int i = 1; i < 100000; ++i) {
-        const double an = -i * (i - a);
-        b += 2.0;
-        d = an * d + b; if (fabs(d) < tiny) d = tiny;
-        c = b + an / c; if (fabs(c) < tiny) c = tiny;
-        d = 1.0 / d;
-        const double del = d * c;
-        h *= del;
-        if (fabs(del - 1.0) < 1e-16) break;
+/* Evaluate the continued fraction  K = a_1/(b_1 + a_2/(b_2 + a_3/(b_3 + ...)))  by the
+ * fundamental (Wallis) recurrences A_n = b_n A_{n-1} + a_n A_{n-2}, B_n = b_n B_{n-1} + a_n B_{n-2}
+ * (A_{-1} = 1, A_0 = 0, B_{-1} = 0, B_0 = 1), K_n = A_n / B_n, rescaling (A, B) by a power of two
+ * whenever |B_n| leaves [2^-500, 2^500] (the ratio is unchanged).  Stops when K_n repeats
+ * K_{n-1} to 1e-16 relative.  The coefficient callback gives (a_n, b_n) for n >= 1. */
+typedef void (*cf_coef_fn)(int n, const double *par, double *an, double *bn);
+static double cf_wallis(cf_coef_fn coef, const double *par) {
+    double A2 = 1.0, A1 = 0.0, B2 = 0.0, B1 = 1.0, K = 0.0;
+    for (int n = 1; n < 200000; ++n) {
+        double an, bn;
+        coef(n, par, &an, &bn);
+        const double A = bn * A1 + an * A2, B = bn * B1 + an * B2;
+        A2 = A1; B2 = B1; A1 = A; B1 = B;
+        const double mb = fabs(B1);
+        if (mb > 0x1p500 || (mb < 0x1p-500 && mb > 0.0)) {
+            const double s = ldexp(1.0, -ilogb(B1));
+            A1 *= s; B1 *= s; A2 *= s; B2 *= s;
+        }
+        if (B1 == 0.0) continue;
+        const double Kn = A1 / B1;
+        if (n > 1 && fabs(Kn - K) <= 1e-16 * fabs(Kn)) return Kn;
+        K = Kn;
     }
-    return exp(-x + a * log(x) - lgamma(a)) * h;
+    return K;
+}
+
+/* Legendre's continued fraction for the upper incomplete gamma (DLMF 8.9.2 in its even form):
+ *   Gamma(a,x) = e^{-x} x^a * 1/(x+1-a - 1(1-a)/(x+3-a - 2(2-a)/(x+5-a - ...))),
+ * i.e. a_1 = 1, a_n = -(n-1)(n-1-a) (n >= 2), b_n = x + 2n - 1 - a.  Used for x >= a+1. */
+static void gamma_q_coef(int n, const double *par, double *an, double *bn) {
+    const double a = par[0], x = par[1];
+    *an = (n == 1) ? 1.0 : -(double)(n - 1) * ((double)(n - 1) - a);
+    *bn = x + 2.0 * n - 1.0 - a;
+}
+static double gamma_q_cf(double a, double x) {
+    const double par[2] = {a, x};
+    return exp(a * log(x) - x - lgamma(a)) * cf_wallis(gamma_q_coef, par);
 }
 
 double orc_gamma_p(double a, double x) {
@@ -149,30 +174,26 @@ double orc_chi2_quantile(double w, double m) {
     return 2.0 * exp(t);
 }
 
-/* Continued fraction for the incomplete beta function (modified Lentz). */
-static double betacf(double a, double b, double x) {
-    const double tiny = 1e-300;
-    const double qab = a + b, qap = a + 1.0, qam = a - 1.0;
-    double c = 1.0, d = 1.0 - qab * x / qap;
-    if (fabs(d) < tiny) d = tiny;
-    d = 1.0 / d;
-    double h = d;
-    for (int k = 1; k < 100000; ++k) {
-        const double k2 = 2.0 * k;
-        double aa = k * (b - k) * x / ((qam + k2) * (a + k2));
-        d = 1.0 + aa * d; if (fabs(d) < tiny) d = tiny;
-        c = 1.0 + aa / c; if (fabs(c) < tiny) c = tiny;
-        d = 1.0 / d;
-        h *= d * c;
-        aa = -(a + k) * (qab + k) * x / ((a + k2) * (qap + k2));
-        d = 1.0 + aa * d; if (fabs(d) < tiny) d = tiny;
-        c = 1.0 + aa / c; if (fabs(c) < tiny) c = tiny;
-        d = 1.0 / d;
-        const double del = d * c;
-        h *= del;
-        if (fabs(del - 1.0) < 1e-16) break;
+/* Continued fraction of the incomplete beta function (DLMF 8.17.22):
+ *   I_x(a,b) = x^a (1-x)^b / (a B(a,b)) * 1/(1 + d_1/(1 + d_2/(1 + ...))),
+ *   d_{2m} = m(b-m)x / ((a+2m-1)(a+2m)),  d_{2m+1} = -(a+m)(a+b+m)x / ((a+2m)(a+2m+1)),
+ * converging quickly for x < (a+1)/(a+b+2).  In the a_n/b_n form: a_1 = 1, a_n = d_{n-1}, b_n = 1. */
+static void ibeta_coef(int n, const double *par, double *an, double *bn) {
+    const double a = par[0], b = par[1], x = par[2];
+    *bn = 1.0;
+    if (n == 1) { *an = 1.0; return; }
+    const int k = n - 1;              /* d_k */
+    if (k % 2 == 0) {
+        const double m = 0.5 * k;
+        *an = m * (b - m) * x / ((a + k - 1.0) * (a + k));
+    } else {
+        const double m = 0.5 * (k - 1);
+        *an = -(a + m) * (a + b + m) * x / ((a + 2.0 * m) * (a + 2.0 * m + 1.0));
     }
-    return h;
+}
+static double betacf(double a, double b, double x) {
+    const double par[3] = {a, b, x};
+    return cf_wallis(ibeta_coef, par);
 }
 
 /* Regularized incomplete beta I_x(a,b); xc = 1-x supplied separately for accuracy. */
@@ -267,6 +288,17 @@ void orc_logchi_table(const orc_lattice *L, double m, double *out) {
     for (int64_t l = 0; l < L->M; ++l) out[l] = log(orc_chi2_quantile(orc_lattice_w(L, l, 0), m));
 }
 
+/* Reading A14 (test harness): keys within 1e-12 max(1, |key|) of each other are near-ties, for which
+ * several variable orders are valid.  orc_set_tie_flip(1) sorts every near-tied pair in the opposite
+ * order (the later variable first), so the parity tests can accept a GPU result that matches the
+ * oracle under either order; the default (0) is the stable ascending order of reading A13. */
+static int g_tie_flip = 0;
+void orc_set_tie_flip(int on) { g_tie_flip = on ? 1 : 0; }
+static int key_before(double kj, double ki) {   /* insertion sort: move kj past ki? */
+    if (kj > ki) return 1;
+    return g_tie_flip && fabs(kj - ki) <= 1e-12 * fmax(1.0, fmax(fabs(kj), fabs(ki)));
+}
+
 /* =====================================================================================
  * T_r(b; 0, S, m) — Genz-Bretz separation of variables for the multivariate t in its
  * chi-normal form (reading R-T):  T_r(b;S,m) = E_V[ Phi_r( b sqrt(V/m); S ) ],
@@ -297,7 +329,7 @@ static double tr_core(int r, const double *b, const double *S, double m, const o
     for (int i = 1; i < r; ++i) {   /* stable insertion sort by key */
         const int pi = perm[i];
         int j = i - 1;
-        while (j >= 0 && key[perm[j]] > key[pi]) { perm[j + 1] = perm[j]; --j; }
+        while (j >= 0 && key_before(key[perm[j]], key[pi])) { perm[j + 1] = perm[j]; --j; }
         perm[j + 1] = pi;
     }
     if (min_key_gap) {
@@ -387,6 +419,35 @@ int orc_derive(int p, int q, const double *sigma, const double *delta, double nu
     return ORC_OK;
 }
 
+/* Parity-harness output (tests only; no effect on the E-step): running error bounds of the two
+ * cancelling sums of O7, in the units of e3 / e4.  E1 = c T2 + S'h and E2 = sym(S'(G + T0 I) + c E1')
+ * are sums of terms of either sign; if every integral (T2, T~(k), T(k,t)) and density factor carries a
+ * relative perturbation <= delta, each moment moves by at most delta times the same sum taken over
+ * |terms|:  B1_a = |c_a T2| + sum_k |S'_ak h_k|,  B2_ab = sum_k |S'_ak| (BG_kb + [k = b] T0) + |c_a| B1_b
+ * (BG_kb = |phi_k| (|c~_b T~(k)| + sum |S~'(k) h(k)|)).  bound[0..q) = (m0/rho) B1 / T0,
+ * bound[q + a q + b] = (m0/rho) (B2_ab + B2_ba) / (2 T0).  In the deep tail of a component
+ * (alpha = c / sqrt(S') << 0) B / |moment| grows like alpha^2 (E1) and alpha^4 (E2): the condition
+ * number of the formula (reading P1). */
+static void moment_bounds(int q, const double *c, const double *Sp, const double *h, double T2, double T0,
+                          const double *BG, double fac, double *bound) {
+    double B1[QMAX];
+    for (int a = 0; a < q; ++a) {
+        double s = fabs(c[a] * T2);
+        for (int k = 0; k < q; ++k) s += fabs(Sp[a * q + k] * h[k]);
+        B1[a] = s;
+        bound[a] = fac * s / T0;
+    }
+    double B2[QMAX * QMAX];
+    for (int a = 0; a < q; ++a)
+        for (int b = 0; b < q; ++b) {
+            double s = 0.0;
+            for (int k = 0; k < q; ++k) s += fabs(Sp[a * q + k]) * (BG[k * q + b] + (k == b ? T0 : 0.0));
+            B2[a * q + b] = s + fabs(c[a]) * B1[b];
+        }
+    for (int a = 0; a < q; ++a)
+        for (int b = 0; b < q; ++b) bound[q + a * q + b] = fac * 0.5 * (B2[a * q + b] + B2[b * q + a]) / T0;
+}
+
 /* =====================================================================================
  * O2-O8: one (observation, component) pair.
  * out = [log(2^q t_p T0)  (no log pi),  e1-e2,  e2,  e3 (q),  e4 (q*q)]
@@ -399,7 +460,7 @@ int orc_derive(int p, int q, const double *sigma, const double *delta, double nu
 int orc_pair(int p, int q, const double *y, const double *mu, const double *L_omega,
              const double *A, const double *Lambda, double nu, double kappa,
              const orc_lattice *L, const double *chi_m0, const double *chi_m1,
-             const double *chi_m2, const double *lv_m0, double *out, double *min_key_gap) {
+             const double *chi_m2, const double *lv_m0, double *out, double *min_key_gap, double *bound) {
     double r[PMAX], v[PMAX];
     for (int a = 0; a < p; ++a) r[a] = y[a] - mu[a];
     for (int a = 0; a < p; ++a) {          /* forward solve L v = r; d = |v|^2 */
@@ -484,8 +545,9 @@ int orc_pair(int p, int q, const double *y, const double *mu, const double *L_om
     /* G_kl = phi_k * E[X_l 1{X_-k > 0} | X_k = 0] (first moment of the conditional truncated t):
      *      = phi_k [ c~(k)_l T~(k) + (S~'(k) h(k))_l ],  G_kk = 0,
      * h(k)_t = t_1(0; c~(k)_t, S~'(k)_tt, m0-1) * T_{q-2}(c^(k,t); 0, S^(k,t), m0). */
-    double G[QMAX * QMAX];
+    double G[QMAX * QMAX], BG[QMAX * QMAX];   /* BG: running bound sum |terms| of G (test output) */
     memset(G, 0, sizeof(G));
+    memset(BG, 0, sizeof(BG));
     if (q >= 2) {
         const int q2 = q - 2;
         double Tkt[QMAX][QMAX];
@@ -523,6 +585,11 @@ int orc_pair(int p, int q, const double *y, const double *mu, const double *L_om
                 double s = ct[k][a] * Tk[k];
                 for (int b = 0; b < q1; ++b) s += Stp[k][a * q1 + b] * hk[b];
                 G[k * q + oth[k][a]] = phi[k] * s;
+                if (bound) {
+                    double sb = fabs(ct[k][a] * Tk[k]);
+                    for (int b = 0; b < q1; ++b) sb += fabs(Stp[k][a * q1 + b] * hk[b]);
+                    BG[k * q + oth[k][a]] = fabs(phi[k]) * sb;
+                }
             }
         }
     }
@@ -543,6 +610,7 @@ int orc_pair(int p, int q, const double *y, const double *mu, const double *L_om
     for (int a = 0; a < q; ++a)
         for (int b = 0; b < q; ++b)
             out[3 + q + a * q + b] = fac * 0.5 * (E2[a * q + b] + E2[b * q + a]) / T0;
+    if (bound) moment_bounds(q, c, Sp, h, T2, T0, BG, fac, bound);
     return ORC_OK;
 }
 
@@ -596,7 +664,7 @@ int orc_pair_direct(int p, int q, const double *y, const double *mu, const doubl
     for (int i = 1; i < q; ++i) {
         const int pi = perm[i];
         int j = i - 1;
-        while (j >= 0 && key[perm[j]] > key[pi]) { perm[j + 1] = perm[j]; --j; }
+        while (j >= 0 && key_before(key[perm[j]], key[pi])) { perm[j + 1] = perm[j]; --j; }
         perm[j + 1] = pi;
     }
     if (min_key_gap)
@@ -688,7 +756,7 @@ static double phi_r(int r, const double *b, const double *S, const orc_lattice *
 
 int orc_pair_sn(int p, int q, const double *y, const double *mu, const double *L_omega,
                 const double *A, const double *Lambda, double logdet, const orc_lattice *L,
-                const double *ones, double *out, double *min_key_gap) {
+                const double *ones, double *out, double *min_key_gap, double *bound) {
     double r[PMAX], v[PMAX];
     for (int a = 0; a < p; ++a) r[a] = y[a] - mu[a];
     for (int a = 0; a < p; ++a) {
@@ -743,8 +811,9 @@ int orc_pair_sn(int p, int q, const double *y, const double *mu, const double *L
         for (int k = 0; k < q; ++k) s += Lambda[a * q + k] * h[k];
         E1[a] = s;
     }
-    double G[QMAX * QMAX];
+    double G[QMAX * QMAX], BG[QMAX * QMAX];
     memset(G, 0, sizeof(G));
+    memset(BG, 0, sizeof(BG));
     if (q >= 2) {
         const int q2 = q - 2;
         double Tkt[QMAX][QMAX];
@@ -777,6 +846,11 @@ int orc_pair_sn(int p, int q, const double *y, const double *mu, const double *L
                 double s = ct[k][a] * Tk[k];
                 for (int b = 0; b < q1; ++b) s += St[k][a * q1 + b] * hk[b];
                 G[k * q + oth[k][a]] = phi[k] * s;
+                if (bound) {
+                    double sb = fabs(ct[k][a] * Tk[k]);
+                    for (int b = 0; b < q1; ++b) sb += fabs(St[k][a * q1 + b] * hk[b]);
+                    BG[k * q + oth[k][a]] = fabs(phi[k]) * sb;
+                }
             }
         }
     }
@@ -791,6 +865,7 @@ int orc_pair_sn(int p, int q, const double *y, const double *mu, const double *L
     for (int a = 0; a < q; ++a) out[3 + a] = E1[a] / P;
     for (int a = 0; a < q; ++a)
         for (int b = 0; b < q; ++b) out[3 + q + a * q + b] = 0.5 * (E2[a * q + b] + E2[b * q + a]) / P;
+    if (bound) moment_bounds(q, c, Lambda, h, P, P, BG, 1.0, bound);
     return ORC_OK;
 }
 
@@ -808,6 +883,17 @@ int orc_estep(int64_t n, int p, int q, int g, const double *y,
               const double *delta, const double *nu, const orc_lattice *L,
               int nthreads, int flags, double *pair_out, double *stats, double *loglik,
               double *min_key_gap) {
+    return orc_estep_b(n, p, q, g, y, pi, mu, sigma, delta, nu, L, nthreads, flags, pair_out, stats, loglik,
+                       min_key_gap, NULL);
+}
+
+/* orc_estep plus, per pair, the running error bounds of e3 / e4 (moment_bounds; [n][g][q + q*q],
+ * analytic estimator only, 0 elsewhere) for the parity harness. */
+int orc_estep_b(int64_t n, int p, int q, int g, const double *y,
+                const double *pi, const double *mu, const double *sigma,
+                const double *delta, const double *nu, const orc_lattice *L,
+                int nthreads, int flags, double *pair_out, double *stats, double *loglik,
+                double *min_key_gap, double *bound_out) {
     if (p < 1 || p > PMAX || q < 0 || q > 6 || g < 1 || n < 0) return ORC_EINVAL;
     const int sn = (flags & ORC_FAMILY_SN) != 0;
     const int direct = (flags & ORC_DIRECT) != 0 && q >= 1;
@@ -845,6 +931,8 @@ int orc_estep(int64_t n, int p, int q, int g, const double *y,
     const int64_t CH = 4096;
     double *buf = (double *)malloc(sizeof(double) * (size_t)CH * g * PW);
     double *gaps = (double *)malloc(sizeof(double) * (size_t)CH * g);
+    const int BW = q + q * q;            /* bound width per pair */
+    double *bnd = bound_out ? (double *)calloc((size_t)CH * g * (BW > 0 ? BW : 1), sizeof(double)) : NULL;
     for (int64_t j0 = 0; j0 < n && rc == ORC_OK; j0 += CH) {
         const int64_t cnt = (n - j0 < CH) ? n - j0 : CH;
         int prc = ORC_OK;
@@ -859,10 +947,12 @@ int orc_estep(int64_t n, int p, int q, int g, const double *y,
                                                     cd[i].Lam, nu[i], cd[i].kappa, cd[i].logdet, sn, L, cd[i].chi0,
                                                     cd[i].lv0, buf + (size_t)jj * PW, &gap)
                          : sn ? orc_pair_sn(p, q, y + (size_t)j * p, mu + (size_t)i * p, cd[i].L, cd[i].A,
-                                            cd[i].Lam, cd[i].logdet, L, cd[i].chi0, buf + (size_t)jj * PW, &gap)
+                                            cd[i].Lam, cd[i].logdet, L, cd[i].chi0, buf + (size_t)jj * PW, &gap,
+                                            bnd ? bnd + (size_t)jj * BW : NULL)
                               : orc_pair(p, q, y + (size_t)j * p, mu + (size_t)i * p, cd[i].L, cd[i].A,
                                          cd[i].Lam, nu[i], cd[i].kappa, L, cd[i].chi0, cd[i].chi1,
-                                         cd[i].chi2, cd[i].lv0, buf + (size_t)jj * PW, &gap);
+                                         cd[i].chi2, cd[i].lv0, buf + (size_t)jj * PW, &gap,
+                                         bnd ? bnd + (size_t)jj * BW : NULL);
             gaps[jj] = gap;
             if (r2 != ORC_OK) prc = r2;
         }
@@ -884,6 +974,8 @@ int orc_estep(int64_t n, int p, int q, int g, const double *y,
                 const double *o = buf + (size_t)(jj * g + i) * PW;
                 const double tau = exp(lf[i] - lse);
                 if (min_key_gap && gaps[jj * g + i] < min_key_gap[j * g + i]) min_key_gap[j * g + i] = gaps[jj * g + i];
+                if (bnd)
+                    for (int k = 0; k < BW; ++k) bound_out[((size_t)j * g + i) * BW + k] = bnd[(size_t)(jj * g + i) * BW + k];
                 if (pair_out) {
                     double *po = pair_out + ((size_t)j * g + i) * (PW + 1);
                     po[0] = lf[i];
@@ -914,6 +1006,7 @@ int orc_estep(int64_t n, int p, int q, int g, const double *y,
     if (loglik) *loglik = ll;
     free(buf);
     free(gaps);
+    free(bnd);
     for (int i = 0; i < g; ++i) { free(cd[i].chi0); free(cd[i].chi1); free(cd[i].chi2); free(cd[i].lv0); }
     free(cd);
     return rc;

@@ -65,12 +65,12 @@ int orc_derive(int p, int q, const double *sigma, const double *delta, double nu
 int orc_pair(int p, int q, const double *y, const double *mu, const double *L_omega,
              const double *A, const double *Lambda, double nu, double kappa,
              const orc_lattice *L, const double *chi_m0, const double *chi_m1,
-             const double *chi_m2, const double *lv_m0, double *out, double *min_key_gap);
+             const double *chi_m2, const double *lv_m0, double *out, double *min_key_gap, double *bound);
 
 /* ---- skew-normal pair (CFUSN, reading F1): ones = radius table of 1.0 (normal SOV) ---- */
 int orc_pair_sn(int p, int q, const double *y, const double *mu, const double *L_omega,
                 const double *A, const double *Lambda, double logdet, const orc_lattice *L,
-                const double *ones, double *out, double *min_key_gap);
+                const double *ones, double *out, double *min_key_gap, double *bound);
 
 /* ---- SOV-direct truncated-moment estimator (reading D1); sn: skew-normal family ---- */
 int orc_pair_direct(int p, int q, const double *y, const double *mu, const double *L_omega,
@@ -86,6 +86,15 @@ int orc_estep(int64_t n, int p, int q, int g, const double *y,
               const double *delta, const double *nu, const orc_lattice *L,
               int nthreads, int flags, double *pair_out, double *stats, double *loglik,
               double *min_key_gap);
+/* the same, plus bound_out (may be NULL): [n][g][q+q*q] running error bounds of e3 / e4 (parity
+ * harness, reading P1; analytic estimator only) */
+int orc_estep_b(int64_t n, int p, int q, int g, const double *y,
+                const double *pi, const double *mu, const double *sigma,
+                const double *delta, const double *nu, const orc_lattice *L,
+                int nthreads, int flags, double *pair_out, double *stats, double *loglik,
+                double *min_key_gap, double *bound_out);
+/* reading A14 harness: 1 = sort near-tied reordering keys (within 1e-12 relative) in the opposite order */
+void orc_set_tie_flip(int on);
 
 /* ---- M-step (O11-O12), in place on the parameter arrays ---- */
 int orc_mstep(int p, int q, int g, double n_total, const double *stats,

@@ -75,33 +75,39 @@ __device__ inline double dev_trigamma(double x) {
     return div_fast(num, den) + ser;
 }
 
-// Continued fraction of the regularized incomplete beta (modified Lentz):
-//   I_x(a,b) = x^a (1-x)^b / (a B(a,b)) * cf(a,b,x),  converging fast for x < (a+1)/(a+b+2).
-__device__ inline double dev_betacf(double a, double b, double x) {
-    // reciprocals by div_fast (rcp.approx + Newton, no IEEE slow-path call): |d|, |c| >= fpmin are
-    // normal numbers; the continued fraction needs no correctly rounded division
-    const double fpmin = 1e-300;
-    double c = 1.0;
-    double d = 1.0 - (a + b) * x / (a + 1.0);
-    d = (fabs(d) < fpmin) ? fpmin : d;
-    d = div_fast(1.0, d);
-    double h = d;
-    for (int m = 1; m <= 4000; ++m) {
-        const double m2 = 2.0 * m;
-        const double num_e = m * (b - m) * x * div_fast(1.0, (a + m2 - 1.0) * (a + m2));
-        d = 1.0 + num_e * d; d = (fabs(d) < fpmin) ? fpmin : d; d = div_fast(1.0, d);
-        c = 1.0 + div_fast(num_e, c); c = (fabs(c) < fpmin) ? fpmin : c;
-        h *= d * c;
-        const double num_o = -(a + m) * (a + b + m) * x * div_fast(1.0, (a + m2) * (a + m2 + 1.0));
-        d = 1.0 + num_o * d; d = (fabs(d) < fpmin) ? fpmin : d; d = div_fast(1.0, d);
-        c = 1.0 + div_fast(num_o, c); c = (fabs(c) < fpmin) ? fpmin : c;
-        const double del = d * c;
-        h *= del;
-        if (fabs(del - 1.0) <= 1e-16) break;
+// Continued fractions by the fundamental (Wallis) recurrences
+//   A_n = b_n A_{n-1} + a_n A_{n-2},  B_n = b_n B_{n-1} + a_n B_{n-2},  K_n = A_n / B_n,
+// with (A, B) rescaled by a power of two when |B_n| leaves [2^-400, 2^400].  Convergence is tested
+// without a division per step: |A_n B_{n-1} - A_{n-1} B_n| <= 1e-16 |A_n B_{n-1}|.
+//
+// Incomplete beta (DLMF 8.17.22): I_x(a,b) = x^a (1-x)^b / (a B(a,b)) * cf,
+//   cf = 1/(1 + d_1/(1 + d_2/(1 + ...))), d_{2m} = m(b-m)x/((a+2m-1)(a+2m)),
+//   d_{2m+1} = -(a+m)(a+b+m)x/((a+2m)(a+2m+1)); fast for x < (a+1)/(a+b+2).
+__device__ __forceinline__ void wallis_step(double an, double bn, double &A1, double &A2, double &B1, double &B2) {
+    const double A = fma(bn, A1, an * A2), B = fma(bn, B1, an * B2);
+    A2 = A1; B2 = B1; A1 = A; B1 = B;
+    const double mb = fabs(B1);
+    if (mb > 0x1p400 || mb < 0x1p-400) {
+        const double s = (mb > 0x1p400) ? 0x1p-400 : 0x1p400;
+        A1 *= s; B1 *= s; A2 *= s; B2 *= s;
     }
-    return h;
 }
-
+__device__ inline double dev_betacf(double a, double b, double x) {
+    // n = 1: a_1 = 1, b_1 = 1  ->  A = 1, B = 1
+    double A2 = 0.0, B2 = 1.0, A1 = 1.0, B1 = 1.0;
+    for (int m = 1; m <= 4000; ++m) {
+        const double k2 = 2.0 * m;
+        const double de = m * (b - m) * x * div_fast(1.0, (a + k2 - 1.0) * (a + k2));          // d_{2m}
+        const double d_o = -(a + m) * (a + b + m) * x * div_fast(1.0, (a + k2) * (a + k2 + 1.0));   // d_{2m+1}
+        // d_{2m-1} was applied in the previous round (d_1 at m = 1 below)
+        if (m == 1) wallis_step(-(a + b) * x * div_fast(1.0, a + 1.0), 1.0, A1, A2, B1, B2);   // d_1
+        wallis_step(de, 1.0, A1, A2, B1, B2);
+        const double Ap = A1, Bp = B1;
+        wallis_step(d_o, 1.0, A1, A2, B1, B2);
+        if (fabs(fma(A1, Bp, -Ap * B1)) <= 1e-16 * fabs(A1 * Bp)) break;
+    }
+    return div_fast(A1, B1);
+}
 // log B(m/2, 1/2), the t_1 CDF normaliser; the E-step takes it from CompDev::lbt (per component,
 // df m0, m0+1, m0+2) so the per-pair T_1 evaluations carry no lgamma.
 __device__ inline double dev_t_lbeta(double m) {
@@ -149,20 +155,17 @@ __device__ inline double dev_gamma_series_P(double a, double x, double lga) {
     }
     return sum * exp(a * log(x) - x - lga);
 }
+// Legendre's continued fraction (DLMF 8.9.2, even form): Gamma(a,x) = e^{-x} x^a cf,
+//   cf = 1/(x+1-a - 1(1-a)/(x+3-a - 2(2-a)/(x+5-a - ...))): a_1 = 1, a_n = -(n-1)(n-1-a), b_n = x+2n-1-a.
 __device__ inline double dev_gamma_cf_Q(double a, double x, double lga) {
-    const double fpmin = 1e-300;
-    double b = x + 1.0 - a, c = 1.0 / fpmin, d = div_fast(1.0, b), h = d;
-    for (int k = 1; k < 10000; ++k) {
-        const double an = -k * (k - a);
-        b += 2.0;
-        d = an * d + b; d = (fabs(d) < fpmin) ? fpmin : d;
-        c = b + div_fast(an, c); c = (fabs(c) < fpmin) ? fpmin : c;
-        d = div_fast(1.0, d);
-        const double del = d * c;
-        h *= del;
-        if (fabs(del - 1.0) <= 1e-16) break;
+    double A2 = 1.0, B2 = 0.0, A1 = 0.0, B1 = 1.0;
+    wallis_step(1.0, x + 1.0 - a, A1, A2, B1, B2);
+    for (int n = 2; n < 10000; ++n) {
+        const double Ap = A1, Bp = B1;
+        wallis_step(-double(n - 1) * (double(n - 1) - a), x + 2.0 * n - 1.0 - a, A1, A2, B1, B2);
+        if (fabs(fma(A1, Bp, -Ap * B1)) <= 1e-16 * fabs(A1 * Bp)) break;
     }
-    return exp(a * log(x) - x - lga) * h;
+    return exp(a * log(x) - x - lga) * div_fast(A1, B1);
 }
 // log P(a,x) (upper = 0) or log Q(a,x) (upper = 1); lga = lgamma(a) (computed once by the caller)
 __device__ inline double dev_log_gamma_PQ(double a, double x, int upper, double lga) {

@@ -84,8 +84,10 @@ def test_mstep_q_function_increases_each_cm_block(orc):
     rng = np.random.default_rng(0)
     for _ in range(20):
         assert Q(mu, D + 1e-4 * rng.standard_normal(D.shape), Sig) < base   # Delta block (given mu)
-        E = 1e-4 * rng.standard_normal((p, p))
-        assert Q(mu, D, Sig + E @ E.T + 1e-5 * (E + E.T)) < base              # Sigma block
+        # symmetric perturbation of size 1e-3: Q drops at second order (~1e-6 relative), far above
+        # Q's rounding (~1e-16); the earlier 1e-9-sized step sat at the rounding level of Q
+        E = 1e-3 * rng.standard_normal((p, p))
+        assert Q(mu, D, Sig + 0.5 * (E + E.T)) < base                          # Sigma block
 
 
 def test_aitken_spec_examples(orc):
