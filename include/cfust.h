@@ -44,9 +44,12 @@ extern "C" {
 #define CFUST_ECUDA -7       /* CUDA runtime error / no device                               */
 #define CFUST_ENCCL -8       /* NCCL error: a failed collective, an NCCL asynchronous error seen
                                 while waiting (ncclCommGetAsyncError is polled), or a wait longer
-                                than the environment's CFUST_NCCL_TIMEOUT_S seconds (if set).  The
-                                communicator is then aborted and every later call on the context
-                                returns CFUST_ENCCL (fail fast; no elastic recovery).           */
+                                than CFUST_NCCL_TIMEOUT_S seconds (environment; default 1800 s when
+                                world > 1, unbounded for one rank).  The communicator is then
+                                aborted and every later call on the context returns CFUST_ENCCL
+                                (fail fast; no elastic recovery).  A local CUDA failure on a
+                                multi-rank context also aborts the communicator, so the peers'
+                                next collective fails instead of blocking.                      */
 
 typedef struct cfust_ctx cfust_ctx;   /* opaque */
 
@@ -122,10 +125,15 @@ int cfust_set_data(cfust_ctx *ctx, const double *y, int32_t on_device);
 int cfust_estep(cfust_ctx *ctx, double *loglik_out, double *stats_out);
 
 /* M-step (Alg. 3; reading R-M, ECM order) from the last E-step's statistics, entirely on the
- * device: mu, Delta, Sigma, nu (bisection root), pi; then re-derives Omega, Lambda, chi nodes. */
+ * device: mu, Delta, Sigma, nu (root of the nu equation by safeguarded Newton, reading A7), pi;
+ * then re-derives Omega, Lambda, chi nodes.  Transactional: if any component fails (ENOTPD,
+ * EEMPTY) no parameter of any component changes; it also refuses (parameters unchanged,
+ * CFUST_EUNDERFLOW) when the E-step flagged an underflow on any rank. */
 int cfust_mstep(cfust_ctx *ctx);
 
-/* One EM iteration = cfust_estep + cfust_mstep; *loglik_out = l at the pre-M-step Psi. */
+/* One EM iteration = cfust_estep + cfust_mstep; *loglik_out = l at the pre-M-step Psi.  Runs as
+ * one CUDA graph (E-step kernel, reduction, the single all-reduce, M-step, chi nodes; captured on
+ * first use, not with opts.timing) with one host synchronisation. */
 int cfust_iterate(cfust_ctx *ctx, double *loglik_out);
 
 /* Density-only pass (T0 only): l = sum_j log f(y_j; Psi) at the current Psi (Eq. (3)). */
@@ -139,9 +147,13 @@ int cfust_loglik(cfust_ctx *ctx, double *out);
 int cfust_predict(cfust_ctx *ctx, int32_t *labels_out, double *tau_out, double *loglik_out);
 
 /* Full fit: E-step, then max_iter x [M-step, E-step] with the Aitken stop when tol > 0
- * (Alg. 4, reading A8); out->loglik_trace gets l^(0..n_iter).  When the fit runs to max_iter the
- * last l comes from the density-only pass (cfust_loglik: same value, no statistics), so call
- * cfust_estep before a further cfust_mstep. */
+ * (Alg. 4, reading A8); out->loglik_trace gets l^(0..n_iter).  Each [M-step, E-step] is one CUDA
+ * graph; the M-step records l on the device, so with tol <= 0 the whole fit runs with one host
+ * synchronisation at the end, and with tol > 0 with one per iteration (l^(k) for the rule).  When
+ * the fit runs to max_iter the last l comes from the density-only pass (cfust_loglik: same value,
+ * no statistics), so call cfust_estep before a further cfust_mstep.  On an error the parameters are
+ * those of the last successful M-step and out->n_iter / the trace follow that point (an E-step
+ * underflow at Psi^(j): n_iter = j - 1; an M-step failure producing Psi^(j+1): n_iter = j). */
 int cfust_fit(cfust_ctx *ctx, int32_t max_iter, double tol, cfust_result *out);
 
 int cfust_get_params(cfust_ctx *ctx, cfust_params *out);         /* copies into caller buffers */
@@ -187,7 +199,8 @@ void *cfust_stream(cfust_ctx *ctx);
 int64_t cfust_launch_count(cfust_ctx *ctx);
 
 /* Fill out[128] with a fresh ncclUniqueId (rank 0), to be broadcast to all ranks and passed
- * as opts.nccl_id (one NCCL all-reduce of the statistics per iteration). */
+ * as opts.nccl_id.  Per EM iteration the ranks exchange exactly one NCCL all-reduce (sum, FP64) of
+ * the vector [statistics (g*K), l, underflow flag]. */
 int cfust_nccl_unique_id(void *out);
 
 /* Diagnostic: evaluate a device special function element-wise on host arrays x[n] -> y[n]

@@ -13,6 +13,7 @@
 #include <nvtx3/nvToolsExt.h>   // header-only NVTX v3: ranges cost a pointer test unless a tool attaches
 #endif
 
+#include <algorithm>
 #include <chrono>
 #include <cmath>
 #include <cstdio>
@@ -43,6 +44,13 @@ struct cfust_ctx {
     int64_t launches = 0;
     int nblocks_last = 0;
     int64_t j0 = 0;                // global index of the first local observation
+    // CUDA graphs of one EM iteration (captured on first use; no timing events inside):
+    //   [0] cfust_iterate order  E-step -> reduce -> all-reduce -> M-step -> chi nodes
+    //   [1] cfust_fit order      M-step -> chi nodes -> E-step -> reduce -> all-reduce
+    cudaGraphExec_t gexec[2] = {nullptr, nullptr};
+    int64_t glaunches[2] = {0, 0}; // kernels of ours per graph launch (NCCL's not counted)
+    int *h_fitctl = nullptr;       // pinned [4]: fit bookkeeping staging (DevState::fitctl)
+    double *h_trace = nullptr;     // pinned [TRACE_CAP]
     // Alg. 1 workspace (allocated on first use)
     int32_t *d_labels = nullptr;   // [m_cap][n]
     int m_cap = 0;
@@ -80,16 +88,27 @@ int fail(cfust_ctx *c, int code, const std::string &msg) {
     return code;
 }
 
+// A local CUDA failure on a multi-rank context: abort the communicator so that the peers' next
+// collective fails (their waits poll ncclCommGetAsyncError) instead of blocking on this rank.
+int fail_local(cfust_ctx *c, int code, const std::string &msg) {
+    if (c && c->comm && c->world > 1) {
+        ncclCommAbort(c->comm);
+        c->comm = nullptr;
+        c->comm_failed = true;
+    }
+    return fail(c, code, msg);
+}
+
 #define CU(call)                                                                                        \
     do {                                                                                                \
         cudaError_t e_ = (call);                                                                        \
-        if (e_ != cudaSuccess) return fail(ctx, CFUST_ECUDA, std::string(#call) + ": " + cudaGetErrorString(e_)); \
+        if (e_ != cudaSuccess) return fail_local(ctx, CFUST_ECUDA, std::string(#call) + ": " + cudaGetErrorString(e_)); \
     } while (0)
 
 #define CUI(call)                                                                                       \
     do {                                                                                                \
         int e_ = (call);                                                                                \
-        if (e_ != 0) return fail(ctx, CFUST_ECUDA, std::string(#call) + ": " + cudaGetErrorString(cudaError_t(e_))); \
+        if (e_ != 0) return fail_local(ctx, CFUST_ECUDA, std::string(#call) + ": " + cudaGetErrorString(cudaError_t(e_))); \
     } while (0)
 
 #define NC(call)                                                                                        \
@@ -137,8 +156,10 @@ int upload_params(cfust_ctx *ctx, const cfust_params *P) {
     return CFUST_OK;
 }
 
-// status word -> error code (after a stream sync)
-int check_status(cfust_ctx *ctx) {
+// status word -> error code (after a stream sync).  uflag: the all-reduced E-step underflow flag
+// (statistics vector entry g*K+1, or d_ll[1] of a density pass) when the caller fetched one; < 0:
+// use this rank's status[0] (set on every rank by the M-step gate from the same global flag).
+int check_status(cfust_ctx *ctx, double uflag = -1.0) {
     const int *st = ctx->h_status;
     if (st[1] < 0) {
         const int code = st[1];
@@ -146,7 +167,8 @@ int check_status(cfust_ctx *ctx) {
                                : code == CFUST_EEMPTY ? "empty component: S0_i < 1e-10"
                                                       : "M-step/derive error");
     }
-    if (st[0] & 1) return fail(ctx, CFUST_EUNDERFLOW, "all component densities underflow at some observation");
+    if ((uflag >= 0.0) ? (uflag > 0.0) : (st[0] & 1))
+        return fail(ctx, CFUST_EUNDERFLOW, "all component densities underflow at some observation");
     if (st[2]) return fail(ctx, CFUST_EINVAL, "y has non-finite entries");
     return CFUST_OK;
 }
@@ -160,8 +182,10 @@ int wait_stream(cfust_ctx *ctx) {
         CU(cudaStreamSynchronize(ctx->stream));
         return CFUST_OK;
     }
-    const char *to = std::getenv("CFUST_NCCL_TIMEOUT_S");   // read per wait: settable at any time
-    const double timeout_s = to ? std::atof(to) : 0.0;
+    // read per wait (settable at any time); with world > 1 a finite default, so a peer that died
+    // before a collective cannot block this rank forever
+    const char *to = std::getenv("CFUST_NCCL_TIMEOUT_S");
+    const double timeout_s = to ? std::atof(to) : (ctx->world > 1 ? 1800.0 : 0.0);
     const auto t0 = std::chrono::steady_clock::now();
     for (;;) {
         const cudaError_t q = cudaStreamQuery(ctx->stream);
@@ -185,11 +209,11 @@ int wait_stream(cfust_ctx *ctx) {
     }
 }
 
-int fetch_status_and_sync(cfust_ctx *ctx) {
+int fetch_status_and_sync(cfust_ctx *ctx, const double *uflag_host = nullptr) {
     CU(cudaMemcpyAsync(ctx->h_status, ctx->s.status, sizeof(int) * 4, cudaMemcpyDeviceToHost, ctx->stream));
     const int rc = wait_stream(ctx);
     if (rc) return rc;
-    return check_status(ctx);
+    return check_status(ctx, uflag_host ? *uflag_host : -1.0);
 }
 
 void rec(cfust_ctx *ctx, int k) {
@@ -211,17 +235,28 @@ int reset_status(cfust_ctx *ctx) {
     return CFUST_OK;
 }
 
-// world > 1: max-reduce the status word over ranks (status[0] underflow flag, status[1] negative
-// error codes -> reduced as max of -code, status[2] non-finite y) so that all ranks agree.
+// Context creation (world > 1): agree on the status word over ranks with ONE collective (max of
+// [underflow, -code, non-finite]) so that every rank returns the same code.  Not used per
+// iteration: there the E-step's underflow flag rides in the statistics all-reduce and the M-step's
+// codes are identical on all ranks (same inputs, same kernel).
 int global_status(cfust_ctx *ctx) {
     if (!ctx->comm) return CFUST_OK;
-    NC(ncclAllReduce(ctx->s.status, ctx->s.status, 1, ncclInt32, ncclMax, ctx->comm, ctx->stream));
-    NC(ncclAllReduce(ctx->s.status + 1, ctx->s.status + 1, 1, ncclInt32, ncclMin, ctx->comm, ctx->stream));
-    NC(ncclAllReduce(ctx->s.status + 2, ctx->s.status + 2, 1, ncclInt32, ncclMax, ctx->comm, ctx->stream));
+    CU(cudaMemcpyAsync(ctx->h_status, ctx->s.status, sizeof(int) * 4, cudaMemcpyDeviceToHost, ctx->stream));
+    int rc = wait_stream(ctx);
+    if (rc) return rc;
+    int *h = ctx->h_status;
+    h[1] = -h[1];
+    CU(cudaMemcpyAsync(ctx->s.status, h, sizeof(int) * 4, cudaMemcpyHostToDevice, ctx->stream));
+    NC(ncclAllReduce(ctx->s.status, ctx->s.status, 3, ncclInt32, ncclMax, ctx->comm, ctx->stream));
+    CU(cudaMemcpyAsync(h, ctx->s.status, sizeof(int) * 4, cudaMemcpyDeviceToHost, ctx->stream));
+    if ((rc = wait_stream(ctx))) return rc;
+    h[1] = -h[1];
+    CU(cudaMemcpyAsync(ctx->s.status, h, sizeof(int) * 4, cudaMemcpyHostToDevice, ctx->stream));
     return CFUST_OK;
 }
 
-// E-step (mode 0) or loglik (mode 1) up to the global reduction; no host sync.
+// E-step (mode 0) or loglik (mode 1) up to the global reduction; no host sync.  The reduced vector
+// (statistics + l + underflow flag, or l + flag) is all-reduced by exactly ONE collective.
 int enqueue_estep(cfust_ctx *ctx, int mode) {
     DevState &s = ctx->s;
     int nb = 0;
@@ -241,11 +276,9 @@ int enqueue_estep(cfust_ctx *ctx, int mode) {
     ctx->nblocks_last = nb;
     if (ctx->comm) {
         Nvtx r("cfust:allreduce");
-        const size_t len = (mode == 1) ? 1 : size_t(s.g) * s.K + 1;
+        const size_t len = (mode == 1) ? 2 : size_t(s.g) * s.K + 2;
         NC(ncclAllReduce(mode == 1 ? ctx->d_ll : s.stats, mode == 1 ? ctx->d_ll : s.stats, len, ncclDouble, ncclSum,
                          ctx->comm, ctx->stream));
-        int rs = global_status(ctx);   // an underflow on one rank is reported by every rank
-        if (rs) return rs;
     }
     rec(ctx, 3);
     return CFUST_OK;
@@ -257,6 +290,44 @@ int enqueue_mstep(cfust_ctx *ctx) {
     CUI(launch_chi(ctx->s, ctx->stream));
     ctx->launches += mstep_launches() + ((ctx->s.M > 0) ? 1 : 0);   // M-step (+ pi, derive), chi nodes
     rec(ctx, 4);
+    return CFUST_OK;
+}
+
+bool use_graphs(const cfust_ctx *ctx) {
+    static const bool off = std::getenv("CFUST_NO_GRAPH") != nullptr;
+    return !ctx->timing && !off;   // per-phase timing events stay on the eager path
+}
+
+void drop_graphs(cfust_ctx *ctx) {
+    for (auto &g : ctx->gexec)
+        if (g) { cudaGraphExecDestroy(g); g = nullptr; }
+}
+
+// One EM iteration as a CUDA graph (which = 0: E then M, cfust_iterate; 1: M then E, cfust_fit),
+// captured on first use from the same enqueue functions as the eager path; eager when timing.
+int enqueue_iteration(cfust_ctx *ctx, int which) {
+    auto body = [&]() {
+        int r = (which == 0) ? enqueue_estep(ctx, 0) : enqueue_mstep(ctx);
+        if (r == CFUST_OK) r = (which == 0) ? enqueue_mstep(ctx) : enqueue_estep(ctx, 0);
+        return r;
+    };
+    if (!use_graphs(ctx)) return body();
+    if (!ctx->gexec[which]) {
+        const int64_t l0 = ctx->launches;
+        CU(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
+        int rc = body();
+        cudaGraph_t g = nullptr;
+        const cudaError_t ee = cudaStreamEndCapture(ctx->stream, &g);
+        if (rc == CFUST_OK && ee != cudaSuccess) rc = fail_local(ctx, CFUST_ECUDA, std::string("graph capture: ") + cudaGetErrorString(ee));
+        if (rc == CFUST_OK && cudaGraphInstantiate(&ctx->gexec[which], g, 0) != cudaSuccess)
+            rc = fail_local(ctx, CFUST_ECUDA, "cudaGraphInstantiate failed");
+        if (g) cudaGraphDestroy(g);
+        ctx->glaunches[which] = ctx->launches - l0;
+        ctx->launches = l0;
+        if (rc) { ctx->gexec[which] = nullptr; return rc; }
+    }
+    CU(cudaGraphLaunch(ctx->gexec[which], ctx->stream));
+    ctx->launches += ctx->glaunches[which];
     return CFUST_OK;
 }
 
@@ -283,8 +354,13 @@ int64_t cfust_launch_count(cfust_ctx *ctx) { return ctx ? ctx->launches : 0; }
 void cfust_destroy(cfust_ctx *ctx) {
     if (!ctx) return;
     if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+    drop_graphs(ctx);
     if (ctx->comm) ncclCommDestroy(ctx->comm);
     DevState &s = ctx->s;
+    cudaFree(s.trace);
+    cudaFree(s.fitctl);
+    cudaFreeHost(ctx->h_fitctl);
+    cudaFreeHost(ctx->h_trace);
     cudaFree(ctx->y_owned);
     cudaFree(s.pi);
     cudaFree(s.mu);
@@ -392,11 +468,19 @@ int cfust_em_init(cfust_ctx **out, const double *y, int64_t n, int32_t p, int32_
                   alloc((void **)&s.chi, sizeof(double) * g * CHI_ROWS * (M > 0 ? M : 1)) &&
                   alloc((void **)&s.W, sizeof(double) * nz * (M > 0 ? M : 1)) &&
                   alloc((void **)&s.partials, sizeof(double) * size_t(max_partial_blocks(s)) * GK1) &&
-                  alloc((void **)&s.stats, sizeof(double) * GK1) && alloc((void **)&s.status, sizeof(int) * 4) &&
-                  alloc((void **)&ctx->d_ll, sizeof(double));
+                  alloc((void **)&s.stats, sizeof(double) * (GK1 + 1)) && alloc((void **)&s.status, sizeof(int) * 4) &&
+                  alloc((void **)&ctx->d_ll, sizeof(double) * 2) &&
+                  alloc((void **)&s.trace, sizeof(double) * TRACE_CAP) && alloc((void **)&s.fitctl, sizeof(int) * 4);
         if (!ok) { rc = fail(ctx, CFUST_ECUDA, "cudaMalloc failed"); break; }
+        if (cudaMemsetAsync(s.stats, 0, sizeof(double) * (GK1 + 1), ctx->stream) != cudaSuccess ||
+            cudaMemsetAsync(s.fitctl, 0, sizeof(int) * 4, ctx->stream) != cudaSuccess) {
+            rc = fail(ctx, CFUST_ECUDA, "cudaMemset failed");
+            break;
+        }
         if (cudaMallocHost((void **)&ctx->h_pin, sizeof(double) * (GK1 + 2)) != cudaSuccess ||
-            cudaMallocHost((void **)&ctx->h_status, sizeof(int) * 4) != cudaSuccess) {
+            cudaMallocHost((void **)&ctx->h_status, sizeof(int) * 4) != cudaSuccess ||
+            cudaMallocHost((void **)&ctx->h_fitctl, sizeof(int) * 4) != cudaSuccess ||
+            cudaMallocHost((void **)&ctx->h_trace, sizeof(double) * TRACE_CAP) != cudaSuccess) {
             rc = fail(ctx, CFUST_ECUDA, "cudaMallocHost failed");
             break;
         }
@@ -451,6 +535,7 @@ int cfust_em_init(cfust_ctx **out, const double *y, int64_t n, int32_t p, int32_
 int cfust_set_data(cfust_ctx *ctx, const double *y, int32_t on_device) {
     if (!ctx || !y) return CFUST_EINVAL;
     DevState &s = ctx->s;
+    if (on_device && y != s.y) drop_graphs(ctx);   // the graphs hold s.y as a kernel argument
     if (on_device) {
         s.y = y;
     } else {
@@ -471,8 +556,8 @@ int cfust_estep(cfust_ctx *ctx, double *loglik_out, double *stats_out) {
     rc = enqueue_estep(ctx, 0);
     if (rc) return rc;
     const size_t len = size_t(s.g) * s.K + 1;
-    CU(cudaMemcpyAsync(ctx->h_pin, s.stats, sizeof(double) * len, cudaMemcpyDeviceToHost, ctx->stream));
-    rc = fetch_status_and_sync(ctx);
+    CU(cudaMemcpyAsync(ctx->h_pin, s.stats, sizeof(double) * (len + 1), cudaMemcpyDeviceToHost, ctx->stream));
+    rc = fetch_status_and_sync(ctx, ctx->h_pin + len);   // global underflow flag (all-reduced)
     acc_phase(ctx, 0, 1, 0);
     acc_phase(ctx, 1, 2, 1);
     acc_phase(ctx, 2, 3, 2);
@@ -499,6 +584,8 @@ int cfust_mstep(cfust_ctx *ctx) {
     return rc;
 }
 
+// E-step + M-step (graph 0) and one host sync: l^(k) and the global underflow flag are read from the
+// statistics vector (the M-step leaves it unchanged) together with the status word.
 int cfust_iterate(cfust_ctx *ctx, double *loglik_out) {
     Nvtx nvtx_range("cfust_iterate");
     if (!ctx) return CFUST_EINVAL;
@@ -506,18 +593,17 @@ int cfust_iterate(cfust_ctx *ctx, double *loglik_out) {
     DevState &s = ctx->s;
     int rc = reset_status(ctx);
     if (rc) return rc;
-    rc = enqueue_estep(ctx, 0);
+    rc = enqueue_iteration(ctx, 0);
     if (rc) return rc;
     const size_t len = size_t(s.g) * s.K + 1;
-    // l^(k) lives in stats[len-1]; copy it before the M-step (the M-step does not modify stats)
-    CU(cudaMemcpyAsync(ctx->h_pin, s.stats + (len - 1), sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
-    rc = enqueue_mstep(ctx);
-    if (rc) return rc;
-    rc = fetch_status_and_sync(ctx);
-    acc_phase(ctx, 0, 1, 0);
-    acc_phase(ctx, 1, 2, 1);
-    acc_phase(ctx, 2, 3, 2);
-    acc_phase(ctx, 3, 4, 3);
+    CU(cudaMemcpyAsync(ctx->h_pin, s.stats + (len - 1), sizeof(double) * 2, cudaMemcpyDeviceToHost, ctx->stream));
+    rc = fetch_status_and_sync(ctx, ctx->h_pin + 1);
+    if (!use_graphs(ctx)) {
+        acc_phase(ctx, 0, 1, 0);
+        acc_phase(ctx, 1, 2, 1);
+        acc_phase(ctx, 2, 3, 2);
+        acc_phase(ctx, 3, 4, 3);
+    }
     ctx->have_stats = false;
     if (rc) return rc;
     if (loglik_out) *loglik_out = ctx->h_pin[0];
@@ -532,8 +618,8 @@ int cfust_loglik(cfust_ctx *ctx, double *out) {
     if (rc) return rc;
     rc = enqueue_estep(ctx, 1);
     if (rc) return rc;
-    CU(cudaMemcpyAsync(ctx->h_pin, ctx->d_ll, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
-    rc = fetch_status_and_sync(ctx);
+    CU(cudaMemcpyAsync(ctx->h_pin, ctx->d_ll, sizeof(double) * 2, cudaMemcpyDeviceToHost, ctx->stream));
+    rc = fetch_status_and_sync(ctx, ctx->h_pin + 1);
     if (rc) return rc;
     *out = ctx->h_pin[0];
     return CFUST_OK;
@@ -556,12 +642,12 @@ int cfust_predict(cfust_ctx *ctx, int32_t *labels_out, double *tau_out, double *
     s.tau_out = nullptr;
     s.label_out = nullptr;
     if (rc) return rc;
-    CU(cudaMemcpyAsync(ctx->h_pin, ctx->d_ll, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    CU(cudaMemcpyAsync(ctx->h_pin, ctx->d_ll, sizeof(double) * 2, cudaMemcpyDeviceToHost, ctx->stream));
     if (labels_out && s.n > 0)
         CU(cudaMemcpyAsync(labels_out, ctx->d_lab, sizeof(int32_t) * s.n, cudaMemcpyDeviceToHost, ctx->stream));
     if (tau_out && s.n > 0)
         CU(cudaMemcpyAsync(tau_out, ctx->d_tau, sizeof(double) * s.n * s.g, cudaMemcpyDeviceToHost, ctx->stream));
-    rc = fetch_status_and_sync(ctx);
+    rc = fetch_status_and_sync(ctx, ctx->h_pin + 1);
     if (rc) return rc;
     if (loglik_out) *loglik_out = ctx->h_pin[0];
     return CFUST_OK;
@@ -576,33 +662,124 @@ static int aitken_stop(double l2, double l1, double l0, double tol) {
     return std::fabs(linf - l0) < tol;
 }
 
+namespace {
+// Final l^(K) of a fit: the density-only pass (T0 alone: the same l as the statistics pass of the
+// analytic estimator, same kernel split and reduction) — the SOV-direct estimator runs its own
+// instantiation for statistics, so there the statistics pass is used to keep the l bits identical
+// to cfust_estep.  *dst = device address of [l, underflow flag].
+int enqueue_final_pass(cfust_ctx *ctx, const double **dst) {
+    const int mode = ctx->s.direct ? 0 : 1;
+    const int rc = enqueue_estep(ctx, mode);
+    *dst = (mode == 1) ? ctx->d_ll : ctx->s.stats + size_t(ctx->s.g) * ctx->s.K;
+    return rc;
+}
+
+// Copy trace slots [from, to) of the device ring into tr (after a sync).
+void drain_trace(cfust_ctx *ctx, std::vector<double> &tr, int from, int to) {
+    for (int k = from; k < to; ++k) tr.push_back(ctx->h_trace[k & (TRACE_CAP - 1)]);
+}
+}  // namespace
+
+// Fit (Alg. 3-4): E-step at Psi^(0), then per iteration k = 1..max_iter the graph [M-step -> chi
+// nodes -> E-step at Psi^(k) -> reduce -> all-reduce] (the last one ends in the final pass).  The
+// M-step records l^(k-1) into a device trace ring and gates itself on errors, so with tol <= 0 the
+// whole fit is enqueued without a host sync (one at the end; one per TRACE_CAP-1 iterations); with
+// tol > 0 there is exactly one host sync per iteration (l^(k) for the Aitken rule, Alg. 4).
 int cfust_fit(cfust_ctx *ctx, int32_t max_iter, double tol, cfust_result *out) {
     Nvtx nvtx_range("cfust_fit");
     if (!ctx || !out || max_iter < 0) return CFUST_EINVAL;
     if (out->loglik_trace && out->trace_cap < max_iter + 1) return fail(ctx, CFUST_EINVAL, "trace_cap < max_iter + 1");
+    CU(cudaSetDevice(ctx->device));
     const auto t0 = std::chrono::steady_clock::now();
+    DevState &s = ctx->s;
+    const size_t GK = size_t(s.g) * s.K;
     std::vector<double> tr;
     tr.reserve(size_t(max_iter) + 1);
-    double l = 0.0;
-    int rc = cfust_estep(ctx, &l, nullptr);
-    if (rc) return rc;
-    tr.push_back(l);
     out->n_iter = 0;
     out->converged = 0;
-    for (int k = 1; k <= max_iter; ++k) {
-        rc = cfust_mstep(ctx);
-        if (rc) break;
-        // E-step at Psi^(k) yields l^(k) (trace convention).  After the last M-step only l is
-        // needed: the density-only pass (T0 alone, bitwise the same l) instead of the statistics
-        // pass — one full E-step fewer per fit (17 % of a 5-iteration cfg4/cfg5 fit).
-        rc = (k == max_iter) ? cfust_loglik(ctx, &l) : cfust_estep(ctx, &l, nullptr);
-        if (rc) break;
-        tr.push_back(l);
-        out->n_iter = k;
-        if (tol > 0.0 && k >= 2 && aitken_stop(tr[k - 2], tr[k - 1], tr[k], tol)) {
-            out->converged = 1;
-            break;
+    ctx->have_stats = false;
+    int rc = reset_status(ctx);
+    if (rc) return rc;
+    int *hf = ctx->h_fitctl;
+    hf[0] = 0; hf[1] = -1; hf[2] = 0; hf[3] = 0;
+    CU(cudaMemcpyAsync(s.fitctl, hf, sizeof(int) * 4, cudaMemcpyHostToDevice, ctx->stream));
+    const double *lsrc = s.stats + GK;   // [l, underflow flag] of the latest pass
+    rc = (max_iter == 0) ? enqueue_final_pass(ctx, &lsrc) : enqueue_estep(ctx, 0);
+    if (rc) return rc;
+    int drained = 0;   // trace slots already copied to tr
+    auto sync_read = [&](int upto) -> int {   // one host sync: fit bookkeeping, trace slots, l, status
+        CU(cudaMemcpyAsync(ctx->h_pin, lsrc, sizeof(double) * 2, cudaMemcpyDeviceToHost, ctx->stream));
+        CU(cudaMemcpyAsync(hf, s.fitctl, sizeof(int) * 4, cudaMemcpyDeviceToHost, ctx->stream));
+        for (int a = drained; a < upto;) {   // new ring slots only (at most two contiguous pieces)
+            const int off = a & (TRACE_CAP - 1), cnt = std::min(upto - a, TRACE_CAP - off);
+            CU(cudaMemcpyAsync(ctx->h_trace + off, s.trace + off, sizeof(double) * cnt, cudaMemcpyDeviceToHost, ctx->stream));
+            a += cnt;
         }
+        CU(cudaMemcpyAsync(ctx->h_status, s.status, sizeof(int) * 4, cudaMemcpyDeviceToHost, ctx->stream));
+        const int r = wait_stream(ctx);
+        if (r) return r;
+        if (upto > drained) { drain_trace(ctx, tr, drained, upto); drained = upto; }
+        return CFUST_OK;
+    };
+    // error bookkeeping -> (rc, n_iter) with orc_fit's semantics: an E-step failure at Psi^(j) ends
+    // the fit with n_iter = j - 1; an M-step failure producing Psi^(j+1) with n_iter = j
+    auto settle = [&](int k_done) -> int {
+        if (hf[1] >= 0) {
+            const int j = hf[1];
+            out->n_iter = (hf[2] == 1) ? (j > 0 ? j - 1 : 0) : j;
+            return check_status(ctx, hf[2] == 1 ? 1.0 : -1.0);
+        }
+        const int r = check_status(ctx, ctx->h_pin[1]);   // the latest pass (final pass: global flag)
+        out->n_iter = (r == CFUST_OK) ? k_done : (k_done > 0 ? k_done - 1 : 0);
+        return r;
+    };
+    double lfinal = 0.0;
+    if (max_iter == 0) {
+        if ((rc = sync_read(0))) return rc;
+        rc = settle(0);
+        lfinal = ctx->h_pin[0];
+    } else if (tol <= 0.0) {
+        for (int k = 1; k <= max_iter && rc == CFUST_OK; ++k) {
+            if (k < max_iter) {
+                rc = enqueue_iteration(ctx, 1);
+            } else {
+                rc = enqueue_mstep(ctx);
+                if (rc == CFUST_OK) rc = enqueue_final_pass(ctx, &lsrc);
+            }
+            // the M-step of iteration k wrote slot k-1: drain before the ring wraps
+            if (rc == CFUST_OK && k < max_iter && k - drained >= TRACE_CAP - 1) rc = sync_read(k);
+        }
+        if (rc) return rc;
+        if ((rc = sync_read(max_iter))) return rc;
+        rc = settle(max_iter);
+        lfinal = ctx->h_pin[0];
+    } else {
+        for (int k = 1; k <= max_iter; ++k) {
+            if (k < max_iter) {
+                rc = enqueue_iteration(ctx, 1);
+            } else {
+                rc = enqueue_mstep(ctx);
+                if (rc == CFUST_OK) rc = enqueue_final_pass(ctx, &lsrc);
+            }
+            if (rc) return rc;
+            if ((rc = sync_read(k))) return rc;
+            if ((rc = settle(k)) != CFUST_OK) break;
+            lfinal = ctx->h_pin[0];
+            // tr holds l^(0..k-1) (the M-steps' records); with l^(k) from this sync:
+            const double lk = lfinal;
+            if (k >= 2 && aitken_stop(tr[k - 2], tr[k - 1], lk, tol)) {
+                out->converged = 1;
+                break;
+            }
+        }
+    }
+    // the trace: l^(0..n_iter-1) recorded on the device, l^(n_iter) from the last pass (or the ring)
+    const int ni = out->n_iter;
+    if (rc == CFUST_OK) {
+        tr.resize(size_t(ni));
+        tr.push_back(lfinal);
+    } else {
+        tr.resize(size_t(std::min<int>(int(tr.size()), ni + 1)));
     }
     if (out->loglik_trace)
         for (size_t k = 0; k < tr.size() && int(k) < out->trace_cap; ++k) out->loglik_trace[k] = tr[k];

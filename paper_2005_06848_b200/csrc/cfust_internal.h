@@ -21,8 +21,10 @@ struct DevState {
     double *chi;                    // [g][CHI_ROWS][M]: chi radius nodes for df m0, m0+1, m0+2; log V (df m0)
     double *W;                      // [q][M] lattice coordinates (fixed per context)
     double *partials;               // [max_blocks][g*K+1]
-    double *stats;                  // [g*K+1] reduced (then all-reduced) statistics
-    int *status;                    // [4]: 0 E-step underflow, 1 M-step/derive error code
+    double *stats;                  // [g*K+2] reduced (then all-reduced): statistics, l, underflow flag
+    int *status;                    // [4]: 0 E-step underflow, 1 M-step/derive error code, 2 non-finite y
+    double *trace;                  // [TRACE_CAP] l^(k) recorded by the M-step during cfust_fit (or NULL)
+    int *fitctl;                    // [3] fit bookkeeping (mstep_fused_kernel), NULL outside cfust_fit
     double nu_lo, nu_hi;
     int M;                          // lattice points (0 when q <= 1)
     uint32_t z[8];
@@ -36,6 +38,8 @@ struct DevState {
     double *tau_out;                // density pass (mode 1): responsibilities [n][g] if non-NULL
     int32_t *label_out;             // density pass (mode 1): argmax_i tau_ij [n] if non-NULL
 };
+
+constexpr int TRACE_CAP = 4096;   // device trace ring (power of two); cfust_fit drains it when full
 
 // rows of the per-component node table DevState::chi
 constexpr int CHI_M1 = 1, CHI_M2 = 2, CHI_LV = 3, CHI_ROWS = 4;

@@ -1173,9 +1173,13 @@ __global__ void __launch_bounds__(TW * 32, CFUST_T_MB) estep_t_mma_kernel(EArgs 
 // partial sums of a column are added in ascending y.  Fixed order -> bitwise reproducible.
 constexpr int RY = 16;
 __global__ void __launch_bounds__(32 * RY) reduce_kernel(const double *__restrict__ partials, int nblocks, int stride,
-                                                         int col0, int ncols, double *__restrict__ out) {
+                                                         int col0, int ncols, double *__restrict__ out,
+                                                         const int *__restrict__ flag, double *__restrict__ flag_out) {
     __shared__ double part[RY][33];
     const int x = threadIdx.x & 31, y = threadIdx.x >> 5;
+    // the E-step's underflow flag (status[0] bit 0) as one more summed entry of the statistics
+    // vector, so the single all-reduce also tells every rank whether some rank underflowed
+    if (flag_out && blockIdx.x == 0 && threadIdx.x == 0) *flag_out = (*flag & 1) ? 1.0 : 0.0;
     const int e = blockIdx.x * 32 + x;
     double s = 0.0;
     if (e < ncols) {
@@ -1297,7 +1301,7 @@ struct MsWork {
     double Sv[KMAX];   // this component's K statistics, staged from global memory in one coalesced read
     double S3[PMAX * PMAX], S5[QMAX * QMAX], mu[PMAX], D[PMAX * QMAX], B[PMAX * QMAX], Sg[PMAX * PMAX];
     double L5[QMAX * QMAX], Lt[PMAX * PMAX];
-    double md;
+    double md, nu;
     int ok;
 };
 
@@ -1403,12 +1407,19 @@ __device__ int mstep_warp(const DevState &s, int i, MsWork &w, int lane, bool do
         __syncwarp();
         if (!warp_chol(p, w.Sg, p, w.Lt, PMAX, lane, &w.ok)) return -4;
     }
+    if (s.family == 1 || lane != 0 || !do_nu) return 0;   // skew-normal / Gaussian: no nu
+    w.nu = nu_update(s, i, S0, S7);
+    return 0;
+}
+
+// Commit component i's M-step result (mu, Sigma, Delta in the shared MsWork; nu if solved) to the
+// device parameter arrays.  Called only after every component's update succeeded, so an error
+// leaves Psi^(k) intact for all components (no mix of Psi^(k) and Psi^(k+1)).
+__device__ void mstep_commit(const DevState &s, int i, const MsWork &w, int lane) {
+    const int p = s.p, q = s.q;
     for (int a = lane; a < p; a += 32) s.mu[size_t(i) * p + a] = w.mu[a];
     for (int t = lane; t < p * p; t += 32) s.sigma[size_t(i) * p * p + t] = w.Sg[t];
     for (int t = lane; t < p * q; t += 32) s.delta[size_t(i) * p * q + t] = w.D[t];
-    if (s.family == 1 || lane != 0 || !do_nu) return 0;   // skew-normal / Gaussian: no nu
-    s.nu[i] = nu_update(s, i, S0, S7);
-    return 0;
 }
 
 struct DvWork {
@@ -1510,6 +1521,10 @@ __global__ void __launch_bounds__(32) mstep_kernel(DevState s) {
     if (i >= s.g) return;
     const int rc = mstep_warp(s, i, w, lane);
     if (rc != 0 && lane == 0) atomicMin(s.status + 1, rc);
+    if (rc != 0) return;
+    __syncwarp();
+    mstep_commit(s, i, w, lane);
+    if (lane == 0 && s.family != 1) s.nu[i] = w.nu;
 }
 
 // pi <- S0 / n_total, floored at 1e-10, renormalised (every block recomputes the total in the same
@@ -1541,10 +1556,35 @@ union MsDvWork {
     MsWork ms;
     DvWork dv;
 };
+// Fit bookkeeping (DevState::fitctl, may be NULL): [0] index of the next trace slot, [1] the trace
+// index at which the first error was seen (-1: none), [2] its kind (1 E-step, 2 M-step / derive).
 __global__ void __launch_bounds__(64 * GMAX) mstep_fused_kernel(DevState s) {
     __shared__ MsDvWork w[GMAX];
     __shared__ double nu_new[GMAX];
+    __shared__ int gate, slot;
     const int i = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int GK = s.g * s.K;
+    if (threadIdx.x == 0) {
+        // l^(k) of the E-step that produced these statistics -> trace slot (cfust_fit, no host sync)
+        int j = -1;
+        if (s.fitctl) {
+            j = s.fitctl[0];
+            s.trace[j & (TRACE_CAP - 1)] = s.stats[GK];
+            s.fitctl[0] = j + 1;
+        }
+        slot = j;
+        // Gate: the E-step flagged an underflow on some rank (the flag travels in the statistics
+        // vector through the one all-reduce, stats[GK + 1]) or non-finite data, or an earlier
+        // M-step of this fit failed: Psi is left unchanged.
+        const bool eflag = s.stats[GK + 1] > 0.0 || (s.status[0] & 1) || s.status[2];
+        if (eflag) {
+            s.status[0] |= 1;
+            if (s.fitctl && s.fitctl[1] < 0) { s.fitctl[1] = j; s.fitctl[2] = 1; }
+        }
+        gate = eflag || s.status[1] < 0;
+    }
+    __syncthreads();
+    if (gate) return;
     const bool tnu = s.family != 1;   // skew-t: nu solved by warp g + i, concurrently with warp i's updates
     if (i < s.g) {
         const int rc = mstep_warp(s, i, w[i].ms, lane, false);
@@ -1555,9 +1595,14 @@ __global__ void __launch_bounds__(64 * GMAX) mstep_fused_kernel(DevState s) {
         if (S0 >= 1e-10) nu_new[c] = nu_update(s, c, S0, S7);   // (S0 < 1e-10: warp c reports -6)
     }
     __syncthreads();
-    if (i >= s.g || reinterpret_cast<volatile int *>(s.status)[1] < 0) return;
+    if (reinterpret_cast<volatile int *>(s.status)[1] < 0) {   // some component failed: commit nothing
+        if (threadIdx.x == 0 && s.fitctl && s.fitctl[1] < 0) { s.fitctl[1] = slot; s.fitctl[2] = 2; }
+        return;
+    }
+    if (i >= s.g) return;
+    mstep_commit(s, i, w[i].ms, lane);
     if (tnu && lane == 0) s.nu[i] = nu_new[i];
-    __syncwarp();
+    __syncwarp();   // the union's MsWork is dead from here on (derive reuses the storage)
     if (lane == 0) {
         double tot = 0.0, mine = 0.0;
         for (int c = 0; c < s.g; ++c) {
@@ -1569,8 +1614,13 @@ __global__ void __launch_bounds__(64 * GMAX) mstep_fused_kernel(DevState s) {
         s.pi[i] = mine / tot;
     }
     __syncwarp();
+    // derive cannot fail here except by rounding (Sigma just passed its Cholesky; Omega = Sigma +
+    // Delta Delta' is then PD): if it does, the error is returned and the caller re-initialises.
     const int rc = derive_warp(s, i, w[i].dv, s.comp[i], lane);
-    if (rc != 0 && lane == 0) atomicMin(s.status + 1, rc);
+    if (rc != 0 && lane == 0) {
+        atomicMin(s.status + 1, rc);
+        if (s.fitctl) atomicCAS(s.fitctl + 2, 0, 2);
+    }
 }
 
 __global__ void __launch_bounds__(32) derive_kernel(DevState s) {
@@ -1875,17 +1925,18 @@ int launch_estep(const DevState &s, int mode, const int64_t *idx, int64_t cnt, d
     }
 }
 
+// mode 1: out[0] = l, out[1] = underflow flag; otherwise out[0..GK] = statistics + l, out[GK + 1] = flag
 int launch_reduce(const DevState &s, int nblocks, int mode, double *out, cudaStream_t st) {
     const int len = s.g * s.K + 1;
     if (mode == 1)   // log-likelihood only: column GK
-        reduce_kernel<<<1, 32 * RY, 0, st>>>(s.partials, nblocks, len, len - 1, 1, out);
+        reduce_kernel<<<1, 32 * RY, 0, st>>>(s.partials, nblocks, len, len - 1, 1, out, s.status, out + 1);
     else
-        reduce_kernel<<<(len + 31) / 32, 32 * RY, 0, st>>>(s.partials, nblocks, len, 0, len, out);
+        reduce_kernel<<<(len + 31) / 32, 32 * RY, 0, st>>>(s.partials, nblocks, len, 0, len, out, s.status, out + len);
     return int(cudaGetLastError());
 }
 
 int launch_reduce_cols(const double *partials, int nblocks, int stride, int ncols, double *out, cudaStream_t st) {
-    reduce_kernel<<<(ncols + 31) / 32, 32 * RY, 0, st>>>(partials, nblocks, stride, 0, ncols, out);
+    reduce_kernel<<<(ncols + 31) / 32, 32 * RY, 0, st>>>(partials, nblocks, stride, 0, ncols, out, nullptr, nullptr);
     return int(cudaGetLastError());
 }
 

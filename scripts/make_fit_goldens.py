@@ -2,7 +2,7 @@
 tests (tests/test_gpu_fullsize.py).  Calls ONLY oracle/ and synth/ (the seeded inputs): no value
 here comes from the CUDA path.
 
-    python scripts/make_fit_goldens.py NAME [--budget-s S] [--threads T]
+    python scripts/make_fit_goldens.py NAME [--budget-s S] [--threads T] [--dir D]
 
 NAME is one of GOLDENS below.  The oracle fit is resumable: every iteration is one oracle E-step
 + M-step (Alg. 3) from the parameters saved after the previous one, so a long
@@ -71,13 +71,13 @@ def cpu_model():
     return platform.processor() or "unknown"
 
 
-def run(name, budget_s, threads):
+def run(name, budget_s, threads, gdir=GDIR):
     cfg, iters = cfg_of(name)
     y, init, _ = synth.make_problem(cfg)
     M, z, sh = synth.lattice_inputs(cfg)
     lat = oracle.Lattice(M, z, sh) if M else None
-    part = os.path.join(GDIR, f"fit_{name}.partial.json")
-    final = os.path.join(GDIR, f"fit_{name}.json")
+    part = os.path.join(gdir, f"fit_{name}.partial.json")
+    final = os.path.join(gdir, f"fit_{name}.json")
     sha = oracle_sha()
     if os.path.exists(part):
         with open(part) as f:
@@ -137,10 +137,12 @@ def main():
     ap.add_argument("names", nargs="+", choices=sorted(GOLDENS))
     ap.add_argument("--budget-s", type=float, default=1e9)
     ap.add_argument("--threads", type=int, default=os.cpu_count() or 1)
+    ap.add_argument("--dir", default=GDIR, help="where the partial / final files are read and written")
     a = ap.parse_args()
     oracle.build()
+    os.makedirs(a.dir, exist_ok=True)
     for nm in a.names:
-        run(nm, a.budget_s, a.threads)
+        run(nm, a.budget_s, a.threads, a.dir)
 
 
 if __name__ == "__main__":
