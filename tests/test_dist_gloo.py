@@ -2,7 +2,8 @@
 ncclUniqueId broadcast helper, and the algebra of one all-reduce of the sufficient statistics
 per iteration followed by the replicated M-step (Alg. 2-3).  The E-step /
 M-step arithmetic here is the oracle's (CUDA kernels need a GPU); the sharding, the exchange
-and the max-over-ranks timing are the product's code (paper_2005_06848_b200.dist)."""
+and the max-over-ranks timing are the product's code (paper_2005_06848_b200.dist), driven through
+the same bootstrap / Ranks calls bench.py makes."""
 import os
 import socket
 
@@ -26,36 +27,41 @@ def _worker(rank, world, port, out_dir):
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     sys.path.insert(0, root)
     import torch
-    import torch.distributed as dist
     import oracle
     import synth as S
     from paper_2005_06848_b200 import dist as D
-    os.environ["MASTER_ADDR"] = "127.0.0.1"
-    os.environ["MASTER_PORT"] = str(port)
-    dist.init_process_group("gloo", rank=rank, world_size=world)
+    # the torchrun environment bench.py reads (D.env_rank), then bench.py's own bootstrap
+    os.environ.update({"MASTER_ADDR": "127.0.0.1", "MASTER_PORT": str(port), "RANK": str(rank),
+                       "WORLD_SIZE": str(world), "LOCAL_RANK": str(rank)})
+    rk = D.bootstrap("gloo")
     try:
-        uid = D.broadcast_unique_id(dist, rank, device="cpu", make_id=lambda: bytes(range(128)))
+        assert (rk.rank, rk.world, rk.device) == (rank, world, "cpu")
+        uid = rk.nccl_id(make_id=lambda: bytes(range(128)))          # what every CfustEM context receives
         assert uid == bytes(range(128))
         cfg = S.with_n(S.CONFIGS[1], 301)
         y, init, _ = S.make_problem(cfg)
         M, z, sh = S.lattice_inputs(cfg)
         lat = oracle.Lattice(M, z, sh)
-        j0, j1 = D.shard_range(cfg.n, rank, world)
+        j0, j1 = rk.shard(cfg.n)
         assert (j0, j1) == S.shard_range(cfg.n, rank, world)
         params = init
         trace = []
         for it in range(3):
             st = oracle.estep(y[j0:j1], params, cfg.q, lat, nthreads=1)["stats"]
-            t = torch.from_numpy(st.copy())
-            dist.all_reduce(t)                                     # the one exchange per iteration
-            trace.append(float(t[-1]))
-            rc, params = oracle.mstep(t.numpy(), params, cfg.p, cfg.q, cfg.n)
+            # the exchanged vector: [statistics, l, underflow flag], summed by the ONE all-reduce
+            v = np.concatenate([st, [0.0]])
+            t = torch.from_numpy(v.copy())
+            rk.dist.all_reduce(t)                                  # the one exchange per iteration
+            assert float(t[-1]) == 0.0                             # no rank underflowed
+            trace.append(float(t[-2]))
+            rc, params = oracle.mstep(t.numpy()[:-1], params, cfg.p, cfg.q, cfg.n)
             assert rc == 0
-        tmax = D.max_over_ranks(dist, 1.0 + rank, device="cpu")
+        rk.barrier()
+        tmax = rk.max(1.0 + rank)                                  # bench.py's max-over-ranks timing
         assert tmax == float(world)
         np.savez(os.path.join(out_dir, f"r{rank}.npz"), trace=np.array(trace), **params)
     finally:
-        dist.destroy_process_group()
+        rk.close()
 
 
 @pytest.mark.parametrize("world", [2])

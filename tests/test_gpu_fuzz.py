@@ -1,6 +1,7 @@
 """Seeded fuzz parity: random (p, q, g, M, n) with p in 1..8, q in 0..6 (q > p included), g in 1..8,
 ragged n, each family / estimator / e1 option, through the C ABI against the oracle (per-pair
-outputs and the statistics; tolerances as tests/test_gpu_parity.py).  Covers shapes the five
+outputs — every pair, running-bound tolerance and reading A14 ties as tests/test_gpu_parity.py — and
+the statistics at 1e-9).  Covers shapes the five
 BASELINE configs do not (p = 1, 5, 7; q = 5; q > p; g = 1, 6, 7)."""
 import os
 
@@ -8,7 +9,7 @@ import numpy as np
 import pytest
 
 import synth
-from test_gpu_parity import _olat, compare_pairs, compare_stats
+from test_gpu_parity import _olat, check_pairs, compare_stats
 
 pytestmark = pytest.mark.gpu
 
@@ -47,9 +48,9 @@ def test_fuzz_parity(cf, orc, k, p, q, g, M, n, opt):
     lat = synth.lattice_inputs(cfg, e1_exact=opt.get("e1_exact", False), direct=opt.get("estimator") == "direct")
     em = cf.CfustEM(y, g, q, init, lat, **opt)
     got = em.pairs(np.arange(n))
-    ref = orc.estep(y, init, q, _olat(orc, lat), pairs=True, gaps=True, **opt)
+    check_pairs(orc, got, y, init, q, lat, **opt)
+    ref = orc.estep(y, init, q, _olat(orc, lat), **opt)
     assert ref["rc"] == 0
-    compare_pairs(got, ref["pairs"], q, ref["gaps"])
     ll, st = em.estep(want_stats=True)
     compare_stats(st, ref["stats"], p, q, g)
     em.close()

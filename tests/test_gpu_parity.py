@@ -2,13 +2,20 @@
 
 Tolerances (BASELINE.json north_star): 1e-9 relative on tau, e2-e4 and the log-likelihood;
 1e-7 on parameters after the EM iterations.  Floors where a relative comparison is undefined:
-log f and log-likelihood compare |d log| <= 1e-9 max(1, |ref|); e3/e4 entries are compared
-relative to the pair's largest |e3| / |e4| entry (cancellation in E1 = c T2 + S'h can make a
-single entry ~0); statistics relative to the largest |entry| of the same S-block.
-Pairs whose variable-reordering keys are within 1e-10 (oracle diagnostic, reading A14) are
-excluded from element-wise comparison — several orders are then valid.  Per-pair e3/e4 of pairs
-with responsibility tau < 1e-30 (no statistic can see them at 1e-9) are compared at 1e-6: in the
-deep tail the analytic E2 route is ill-conditioned on both sides (reading P1).
+log f and log-likelihood compare |d log| <= 1e-9 max(1, |ref|); statistics relative to the
+largest |entry| of the same S-block.
+
+Per-pair e3 / e4 entries (check_pairs): |gpu - oracle| <= 1e-9 s + DELTA B, with s the pair's
+largest |e3| (|e4|) entry and B the oracle's running error bound of the entry (moment_bounds in
+oracle/cfust_oracle.c: the same sums taken over |terms|).  DELTA = 1e-12 is the relative agreement
+of the two sides' T-integrals and densities (independently rounded special functions; DESIGN.md
+reading P1): B/s is the condition number of E1 = c T2 + S'h and E2 = sym(S'(G + T0 I) + c E1'),
+O(1) for ordinary pairs (the bound is then 1e-9 s) and ~alpha^4 in a component's deep tail, where
+the formula itself cancels on both sides.  Every pair is compared — no responsibility cut-off.
+
+Near ties (reading A14): a pair whose reordering keys are within 1e-12 max(1, |key|) has several
+valid variable orders; if it fails under the oracle's order it must match the oracle evaluated with
+every near tie in the opposite order (orc_set_tie_flip).  Exact ties (gap 0) are compared as is.
 """
 import numpy as np
 import pytest
@@ -18,8 +25,8 @@ import synth
 pytestmark = pytest.mark.gpu
 
 TOL = 1e-9
-TAU_TAIL = 1e-30   # responsibility below which a pair cannot affect any statistic at 1e-9
-TAIL_TOL = 1e-6
+DELTA = 1e-12      # relative agreement of the two sides' integrals (reading P1)
+NEAR_TIE = 1e-12   # reading A14
 PTOL = 1e-7
 
 
@@ -57,40 +64,55 @@ def _olat(orc, lat):
     return orc.Lattice(M, z, sh) if M else None
 
 
-def compare_pairs(got, ref, q, gaps=None, tol=TOL):
-    """got/ref: [n, g, 4+q+q*q] = logf, tau, e1me2, e2, e3(q), e4(q*q)."""
-    ok = np.ones(got.shape[:2], bool) if gaps is None else gaps > 1e-10
-    assert ok.mean() > 0.95, f"too many near-tie pairs: {(~ok).sum()}"
-    g_, r_ = got[ok], ref[ok]
-    fin = np.isfinite(r_[:, 0])
-    assert np.array_equal(fin, np.isfinite(g_[:, 0]))
-    g_, r_ = g_[fin], r_[fin]
-    errs = {}
-    errs["logf"] = np.max(np.abs(g_[:, 0] - r_[:, 0]) / np.maximum(1.0, np.abs(r_[:, 0])))
-    errs["tau"] = np.max(np.abs(g_[:, 1] - r_[:, 1]) / np.maximum(np.abs(r_[:, 1]), 1e-300))
-    # (skew-normal family: e1 - e2 = 0 and e2 = 1 exactly on both sides)
-    errs["e1me2"] = np.max(np.abs(g_[:, 2] - r_[:, 2]) / np.maximum(np.abs(r_[:, 2]), 1e-300))
-    errs["e2"] = np.max(np.abs(g_[:, 3] - r_[:, 3]) / np.maximum(np.abs(r_[:, 3]), 1e-300))
-    if q:
-        # Weight-bearing pairs (tau >= TAU_TAIL) at tol.  Pairs with tau < TAU_TAIL cannot move any
-        # statistic (tau * e) at the 1e-9 level; their E2 = S'(G + T0 I) + c E1' cancels like c^2
-        # in the deep tail (relative conditioning ~ alpha^4 eps, alpha = c / sqrt(S)), so both
-        # sides agree only to ~1e-9..1e-8 there (DESIGN.md reading P1; profiles/r01_fuzz_wide.log):
-        # compared at TAIL_TOL.
-        live = r_[:, 1] >= TAU_TAIL
-        e3g, e3r = g_[:, 4:4 + q], r_[:, 4:4 + q]
-        s3 = np.max(np.abs(e3r), axis=1, keepdims=True)
-        r3 = np.max(np.abs(e3g - e3r) / s3, axis=1)
-        e4g, e4r = g_[:, 4 + q:], r_[:, 4 + q:]
-        s4 = np.max(np.abs(e4r), axis=1, keepdims=True)
-        r4 = np.max(np.abs(e4g - e4r) / s4, axis=1)
-        errs["e3"] = np.max(r3[live], initial=0.0)
-        errs["e4"] = np.max(r4[live], initial=0.0)
-        errs["e3_tail"] = np.max(r3[~live], initial=0.0)
-        errs["e4_tail"] = np.max(r4[~live], initial=0.0)
-    bad = {k: v for k, v in errs.items() if not v <= (TAIL_TOL if k.endswith("_tail") else tol)}
-    assert not bad, f"parity errors {bad} (all: {errs})"
-    return errs
+def _normalized_pair_errors(got, ref, bounds, q, tol):
+    """Per (observation, component): max over the outputs of |gpu - oracle| / allowed (pass <= 1),
+    and the per-quantity maxima for the report."""
+    fin = np.isfinite(ref[..., 0])
+    assert np.array_equal(fin, np.isfinite(got[..., 0])), "underflow pattern (log f = -inf) differs"
+    with np.errstate(invalid="ignore", divide="ignore"):
+        parts = {
+            "logf": np.abs(got[..., 0] - ref[..., 0]) / (tol * np.maximum(1.0, np.abs(ref[..., 0]))),
+            "tau": np.abs(got[..., 1] - ref[..., 1]) / (tol * np.maximum(np.abs(ref[..., 1]), 1e-300)),
+            # (skew-normal family: e1 - e2 = 0 and e2 = 1 exactly on both sides)
+            "e1me2": np.abs(got[..., 2] - ref[..., 2]) / (tol * np.maximum(np.abs(ref[..., 2]), 1e-300)),
+            "e2": np.abs(got[..., 3] - ref[..., 3]) / (tol * np.maximum(np.abs(ref[..., 3]), 1e-300)),
+        }
+        if q:
+            B = np.zeros(got.shape[:2] + (q + q * q,)) if bounds is None else bounds
+            for name, sl, bs in (("e3", slice(4, 4 + q), slice(0, q)), ("e4", slice(4 + q, None), slice(q, None))):
+                r = ref[..., sl]
+                s = np.max(np.abs(r), axis=-1, keepdims=True)
+                allowed = tol * s + DELTA * B[..., bs]
+                e = np.abs(got[..., sl] - r)
+                parts[name] = np.max(np.where(e == 0.0, 0.0, e / np.maximum(allowed, 1e-300)), axis=-1)
+    parts["logf"] = np.where(fin, parts["logf"], 0.0)
+    for k in list(parts):
+        parts[k] = np.where(fin, np.nan_to_num(parts[k], nan=np.inf), 0.0) if k != "tau" else np.nan_to_num(parts[k], nan=np.inf)
+    worst = np.max(np.stack(list(parts.values())), axis=0)
+    return worst, {k: float(np.max(v)) * tol for k, v in parts.items()}
+
+
+def check_pairs(orc, got, y, params, q, lat, tol=TOL, **opt):
+    """GPU per-pair outputs got[n, g, 4+q+q*q] (logf, tau, e1-e2, e2, e3, e4) for the rows y[n]
+    at Psi = params against the oracle (module docstring: running-bound tolerance, reading A14 ties).
+    Returns the per-quantity maxima of |gpu - oracle| / allowed * tol."""
+    analytic = opt.get("estimator", "analytic") == "analytic"
+    ref = orc.estep(y, params, q, _olat(orc, lat), pairs=True, gaps=True, bounds=analytic and q > 0, **opt)
+    assert ref["rc"] == 0, ref["rc"]
+    worst, rep = _normalized_pair_errors(got, ref["pairs"], ref.get("bounds"), q, tol)
+    bad = worst > 1.0
+    near = (ref["gaps"] > 0.0) & (ref["gaps"] < NEAR_TIE)
+    retry = np.nonzero(np.any(bad & near, axis=1))[0]
+    if len(retry):
+        ref2 = orc.estep(y[retry], params, q, _olat(orc, lat), pairs=True, bounds=analytic and q > 0, tie_flip=True,
+                         **opt)
+        w2, _ = _normalized_pair_errors(got[retry], ref2["pairs"], ref2.get("bounds"), q, tol)
+        bad[retry] &= ~(near[retry] & (w2 <= 1.0))
+    assert not bad.any(), (f"parity errors on {int(bad.sum())} of {bad.size} pairs (first {np.argwhere(bad)[:5].tolist()}); "
+                           f"worst/allowed x tol: {rep}")
+    rep["near_ties"] = int(near.sum())
+    rep["tie_retries"] = int(len(retry))
+    return rep
 
 
 def compare_stats(got, ref, p, q, g, tol=TOL):
@@ -131,8 +153,7 @@ def test_pairs_parity(cf, orc, cfg_id, n):
     cfg, y, init, lat = _problem(cfg_id, n)
     em = cf.CfustEM(y, cfg.g, cfg.q, init, lat)
     got = em.pairs(np.arange(n))
-    ref = orc.estep(y, init, cfg.q, _olat(orc, lat), pairs=True, gaps=True)
-    compare_pairs(got, ref["pairs"], cfg.q, ref["gaps"])
+    check_pairs(orc, got, y, init, cfg.q, lat)
     em.close()
 
 
@@ -198,8 +219,7 @@ def test_full_size_sampled(cf, orc, cfg_id, nsample):
     else:
         idx = np.linspace(0, cfg.n - 1, nsample).astype(np.int64)
         got = em.pairs(idx)
-        ref = orc.estep(y[idx], init, cfg.q, _olat(orc, lat), pairs=True, gaps=True)
-        compare_pairs(got, ref["pairs"], cfg.q, ref["gaps"])
+        check_pairs(orc, got, y[idx], init, cfg.q, lat)
     em.close()
 
 
@@ -220,8 +240,7 @@ def test_q_variants_g1(cf, orc, q):
     cfg, y, init, lat = _problem(1, 257, q=q, g=1, pi_kind="uniform")
     em = cf.CfustEM(y, cfg.g, cfg.q, init, lat)
     got = em.pairs(np.arange(cfg.n))
-    ref = orc.estep(y, init, cfg.q, _olat(orc, lat), pairs=True, gaps=True)
-    compare_pairs(got, ref["pairs"], cfg.q, ref["gaps"])
+    check_pairs(orc, got, y, init, cfg.q, lat)
     assert np.all(got[:, 0, 1] == 1.0)
     em.close()
 
@@ -299,11 +318,10 @@ def test_e1_exact_pairs_and_stats_parity(cf, orc, cfg_id, n, kw):
     cfg, y, init, lat = _problem_e1(cfg_id, n, **kw)
     em = cf.CfustEM(y, cfg.g, cfg.q, init, lat, e1_exact=True)
     got = em.pairs(np.arange(n))
-    ref = orc.estep(y, init, cfg.q, _olat(orc, lat), pairs=True, gaps=True, e1_exact=True)
-    compare_pairs(got, ref["pairs"], cfg.q, ref["gaps"])
+    check_pairs(orc, got, y, init, cfg.q, lat, e1_exact=True)
     # the e1 column really is the exact one (differs from reading A5 beyond the tolerance)
     a5 = orc.estep(y, init, cfg.q, _olat(orc, lat), pairs=True)["pairs"]
-    assert np.max(np.abs(a5[..., 2] - ref["pairs"][..., 2])) > 1e-6
+    assert np.max(np.abs(a5[..., 2] - got[..., 2])) > 1e-6
     ll, st = em.estep(want_stats=True)
     compare_stats(st, ref["stats"], cfg.p, cfg.q, cfg.g)
     em.close()
@@ -328,10 +346,10 @@ def test_skew_normal_pairs_stats_parity(cf, orc, cfg_id, n):
     cfg, y, init, lat = _problem(cfg_id, n)
     em = cf.CfustEM(y, cfg.g, cfg.q, init, lat, family="sn")
     got = em.pairs(np.arange(n))
-    ref = orc.estep(y, init, cfg.q, _olat(orc, lat), pairs=True, gaps=True, family="sn")
-    compare_pairs(got, ref["pairs"], cfg.q, ref["gaps"])
+    check_pairs(orc, got, y, init, cfg.q, lat, family="sn")
     assert not np.any(got[..., 2]) and np.all(got[..., 3] == 1.0)   # e1 - e2 = 0, e2 = 1 (W = 1)
     ll, st = em.estep(want_stats=True)
+    ref = orc.estep(y, init, cfg.q, _olat(orc, lat), family="sn")
     compare_stats(st, ref["stats"], cfg.p, cfg.q, cfg.g)
     assert abs(ll - ref["loglik"]) <= TOL * abs(ref["loglik"])
     em.close()
@@ -366,8 +384,8 @@ def test_direct_pairs_and_stats_parity(cf, orc, cfg_id, n, kw):
     cfg, y, init, lat = _problem_direct(cfg_id, n, **kw)
     em = cf.CfustEM(y, cfg.g, cfg.q, init, lat, estimator="direct", family=fam)
     got = em.pairs(np.arange(n))
-    ref = orc.estep(y, init, cfg.q, _olat(orc, lat), pairs=True, gaps=True, estimator="direct", family=fam)
-    compare_pairs(got, ref["pairs"], cfg.q, ref["gaps"])
+    check_pairs(orc, got, y, init, cfg.q, lat, estimator="direct", family=fam)
+    ref = orc.estep(y, init, cfg.q, _olat(orc, lat), estimator="direct", family=fam)
     ll, st = em.estep(want_stats=True)
     compare_stats(st, ref["stats"], cfg.p, cfg.q, cfg.g)
     # same density / tau as the analytic estimator
@@ -401,14 +419,12 @@ def test_subnormal_density_pairs(cf, orc, family):
     idx = np.array([45535, 142656, 731696, 976575, 1572711, 2592729])
     em = cf.CfustEM(torch.from_numpy(y).cuda(), cfg.g, cfg.q, init, lat, family=family)
     got = em.pairs(idx)
-    ref = orc.estep(y[idx], init, cfg.q, _olat(orc, lat), pairs=True, gaps=True, family=family)
+    ref = orc.estep(y[idx], init, cfg.q, _olat(orc, lat), pairs=True, family=family)
     assert np.all(np.isfinite(got[..., 1:])) and np.all(np.isfinite(ref["pairs"][..., 1:]))
     assert np.array_equal(np.isfinite(got[..., 0]), np.isfinite(ref["pairs"][..., 0]))
     if family == "sn":
         assert np.all(~np.isfinite(got[:, 5, 0])) and np.all(got[:, 5, 1] == 0.0)   # underflow, tau = 0
-    fin = np.isfinite(ref["pairs"][..., 0])
-    if fin.any():
-        compare_pairs(got[fin][:, None], ref["pairs"][fin][:, None], cfg.q)
+    check_pairs(orc, got, y[idx], init, cfg.q, lat, family=family)
     em.close()
 
 
@@ -428,8 +444,7 @@ def test_full_size_options_finite(cf, orc, cfg_id, opt):
     assert abs(sum(st[i * K] for i in range(cfg.g)) - cfg.n) <= 1e-9 * cfg.n
     idx = np.linspace(0, cfg.n - 1, 6).astype(np.int64)
     got = em.pairs(idx)
-    ref = orc.estep(y[idx], init, cfg.q, _olat(orc, lat), pairs=True, gaps=True, **opt)
-    compare_pairs(got, ref["pairs"], cfg.q, ref["gaps"])
+    check_pairs(orc, got, y[idx], init, cfg.q, lat, **opt)
     em.mstep()
     em.close()
 
@@ -447,16 +462,14 @@ def test_empty_shard_and_max_shapes(cf, orc):
     latm = synth.lattice_inputs(cmax)
     em = cf.CfustEM(y, cmax.g, cmax.q, init, latm)
     got = em.pairs(np.arange(cmax.n))
-    ref = orc.estep(y, init, cmax.q, _olat(orc, latm), pairs=True, gaps=True)
-    compare_pairs(got, ref["pairs"], cmax.q, ref["gaps"])
+    check_pairs(orc, got, y, init, cmax.q, latm)
     em.close()
     cbig = synth.with_(synth.CONFIGS[1], n=9, M=65536)
     y, init, _ = synth.make_problem(cbig)
     latb = synth.lattice_inputs(cbig)
     em = cf.CfustEM(y, cbig.g, cbig.q, init, latb)
     got = em.pairs(np.arange(cbig.n))
-    ref = orc.estep(y, init, cbig.q, _olat(orc, latb), pairs=True, gaps=True)
-    compare_pairs(got, ref["pairs"], cbig.q, ref["gaps"])
+    check_pairs(orc, got, y, init, cbig.q, latb)
     em.close()
 
 
