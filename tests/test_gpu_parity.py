@@ -322,6 +322,7 @@ def test_e1_exact_pairs_and_stats_parity(cf, orc, cfg_id, n, kw):
     # the e1 column really is the exact one (differs from reading A5 beyond the tolerance)
     a5 = orc.estep(y, init, cfg.q, _olat(orc, lat), pairs=True)["pairs"]
     assert np.max(np.abs(a5[..., 2] - got[..., 2])) > 1e-6
+    ref = orc.estep(y, init, cfg.q, _olat(orc, lat), e1_exact=True)
     ll, st = em.estep(want_stats=True)
     compare_stats(st, ref["stats"], cfg.p, cfg.q, cfg.g)
     em.close()
