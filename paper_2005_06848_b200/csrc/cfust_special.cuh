@@ -64,6 +64,47 @@ __device__ __forceinline__ double div_fast(double p, double q) {
     return fma(fma(-q, y, p), r, y);
 }
 
+#ifndef CFUST_DIV_F32
+#define CFUST_DIV_F32 0   // 1: Phi's quotient from an FP32 reciprocal seed (two FP64 Newton steps)
+#endif
+// P / Q for the Mills-ratio rational only (Q in [1, 1e11] on [0, 40]: safe in FP32).
+__device__ __forceinline__ double div_rat(double p, double q) {
+#if CFUST_DIV_F32
+    float rf;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(rf) : "f"(__double2float_rn(q)));
+    double r = double(rf);
+    double e = fma(-q, r, 1.0);
+    r = fma(r, e, r);
+    e = fma(-q, r, 1.0);
+    r = fma(r, e, r);
+    const double y = p * r;
+    return fma(fma(-q, y, p), r, y);
+#else
+    return div_fast(p, q);
+#endif
+}
+
+#ifndef CFUST_HORNER_EO
+#define CFUST_HORNER_EO 0   // 1: even/odd split Horner (two half-length chains per polynomial)
+#endif
+// p(x) = pe(x^2) + x po(x^2) with x2 = x*x supplied by the caller.
+template <int N>
+__device__ __forceinline__ double horner_eo(const double (&c)[N], double x, double x2) {
+#if CFUST_HORNER_EO
+    constexpr int NE = (N + 1) / 2, NO = N / 2;
+    double pe = c[2 * (NE - 1)];
+#pragma unroll
+    for (int k = NE - 2; k >= 0; --k) pe = fma(pe, x2, c[2 * k]);
+    double po = c[2 * (NO - 1) + 1];
+#pragma unroll
+    for (int k = NO - 2; k >= 0; --k) po = fma(po, x2, c[2 * k + 1]);
+    return fma(po, x, pe);
+#else
+    (void)x2;
+    return horner_c(c, x);
+#endif
+}
+
 #ifndef CFUST_OWN_ELEM
 #define CFUST_OWN_ELEM 1   // own branch-free exp/log/sqrt; with the seeded Phi^{-1} 11% faster E-step
 #endif                     // than libdevice (profiles/r01_seed_variants.log)
@@ -144,7 +185,7 @@ __device__ __forceinline__ double exp_neg2(double xh, double xl) {
     const int k = __double2loint(t);
     const double kd = t - 6755399441055744.0;
     const double r = fma(kd, -2.3190468138462996e-17, fma(kd, -0.69314718055994528623, xh)) + xl;
-    const double p = horner_c(c_EXPC, r);
+    const double p = horner_eo(c_EXPC, r, r * r);
     const double res = __hiloint2double(__double2hiint(p) + k * (1 << 20), __double2loint(p));
     return (xh < -708.0) ? 0.0 : res;
 #else
@@ -205,7 +246,7 @@ __device__ __forceinline__ double Phi_fast(double x) {
     const double lo = fma(ax, ax, -hi);
     const double e = exp_neg2(-0.5 * hi, -0.5 * lo);
 #if CFUST_HORNER
-    const double t = e * div_fast(horner_c(c_PH_P, ax), horner_c(c_PH_Q, ax));
+    const double t = e * div_rat(horner_eo(c_PH_P, ax, hi), horner_eo(c_PH_Q, ax, hi));
 #else
     const double x4 = hi * hi, x8 = x4 * x4;
     const double t = e * div_fast(estrin_c(c_PH_P, ax, hi, x4, x8), estrin_c(c_PH_Q, ax, hi, x4, x8));
@@ -299,7 +340,7 @@ __device__ __forceinline__ double Phiinv_seed(double u) {
     const double hi = ax * ax;
     const double lo = fma(ax, ax, -hi);
     const double ep = exp_neg2(0.5 * hi, 0.5 * lo);                         // e^{z0^2/2} (valid to +709)
-    const double R = div_fast(horner_c(c_PH_P, ax), horner_c(c_PH_Q, ax));
+    const double R = div_rat(horner_eo(c_PH_P, ax, hi), horner_eo(c_PH_Q, ax, hi));
     const double r = 2.5066282746310002 * fma(t, ep, -R);
     const double x = fma(r, fma(r, fma(r, fma(hi, 1.0 / 3.0, 1.0 / 6.0), -0.5 * ax), 1.0), -ax);
 #if CFUST_INTSEL
