@@ -991,6 +991,13 @@ __global__ void __launch_bounds__(TT, 2) estep_t_kernel(EArgs A, int mode) {
 #define CFUST_TW 16
 #endif
 constexpr int TW = CFUST_TW;   // warps per block of the q = 0 kernel
+#ifndef CFUST_T_P2
+#define CFUST_T_P2 2        // phase 2: 1 = w by shuffles + S2 by DADD; 2 = w rows in shared memory + S2 by one DMMA
+#endif
+constexpr int WSTR = 10;   // w row stride (doubles): 80-byte rows, 16-byte aligned, conflict-free 4-row reads
+#ifndef CFUST_T_TMA
+#define CFUST_T_TMA 1       // y tiles staged in shared memory by 1-D bulk copies (double-buffered)
+#endif
 #ifndef CFUST_T_MB
 #define CFUST_T_MB 1        // blocks per SM: 16 warps in one block (profiles/r01_cfg3_mma.log)
 #endif
@@ -999,6 +1006,28 @@ __device__ __forceinline__ void dmma_884(double &c0, double &c1, double a, doubl
     asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
                  : "+d"(c0), "+d"(c1)
                  : "d"(a), "d"(b));
+}
+
+// Column b of L_i^{-1} into X (stride PMAX, rows a >= b; zero elsewhere): forward substitution of
+// L X = e_b, row a: X_ab = -(sum_{c=b}^{a-1} L_ac X_cb) / L_aa.
+__device__ __forceinline__ void t_linv_col(const CompDev &cp, int p, int b, double *X) {
+    for (int a = 0; a < PMAX; ++a) {
+        double x = 0.0;
+        if (a < p && b < p && a >= b) {
+            if (a == b) x = cp.Linv[a];
+            else {
+                double r = 0.0;
+                for (int c = b; c < a; ++c) r = fma(cp.L[a * PMAX + c], X[c * PMAX + b], r);
+                x = -r * cp.Linv[a];
+            }
+        }
+        X[a * PMAX + b] = x;
+    }
+}
+__device__ __forceinline__ double t_ml_row(const CompDev &cp, int p, int a, const double *X) {
+    double m = 0.0;
+    for (int b = 0; b <= a && b < p; ++b) m = fma(X[a * PMAX + b], cp.mu[b], m);
+    return m;
 }
 
 template <int G>
@@ -1016,44 +1045,96 @@ __global__ void __launch_bounds__(TW * 32, CFUST_T_MB) estep_t_mma_kernel(EArgs 
     // other (no substitution chain: 9 % faster at cfg3, profiles/r01_cfg3_mma.log).
     double *Li = red + TW * (GK + 1);                    // [G][PMAX*PMAX]
     double *mL = Li + G * PMAX * PMAX;                   // [G][PMAX]
-    __syncthreads();
-    for (int t = threadIdx.x; t < G * PMAX; t += blockDim.x) {
-        const int i = t / PMAX, b = t % PMAX;
-        const CompDev &cp = comp[i];
-        double *X = Li + i * PMAX * PMAX;
-        for (int a = 0; a < PMAX; ++a) {
-            double x = 0.0;
-            if (a < p && b < p && a >= b) {
-                if (a == b) x = cp.Linv[a];
-                else {
-                    double r = 0.0;
-                    for (int c = b; c < a; ++c) r = fma(cp.L[a * PMAX + c], X[c * PMAX + b], r);
-                    x = -r * cp.Linv[a];
-                }
-            }
-            X[a * PMAX + b] = x;
-        }
+#if CFUST_T_TMA
+    // y tiles staged by the TMA engine: per warp two 32-row buffers (double buffering), each with
+    // an mbarrier that the bulk copy completes; the next tile's rows land while this one computes.
+    double *ybuf = reinterpret_cast<double *>((reinterpret_cast<uintptr_t>(mL + G * PMAX) + 127) & ~uintptr_t(127));   // [TW][2][32*PMAX]
+    uint64_t *mbar = reinterpret_cast<uint64_t *>(ybuf + TW * 2 * 32 * PMAX);   // [TW][2]
+    if (lane == 0) {
+        mbar_init(mbar + 2 * wid, 1);
+        mbar_init(mbar + 2 * wid + 1, 1);
+        fence_proxy_async();
     }
+    double *wsm_all = reinterpret_cast<double *>(mbar + 2 * TW);
+#else
+    double *wsm_all = reinterpret_cast<double *>((reinterpret_cast<uintptr_t>(mL + G * PMAX) + 127) & ~uintptr_t(127));
+#endif
+#if CFUST_T_P2 == 2
+    // per warp: 32 rows of this tile's weights w_i = tau_i e2_i (i < G; entries G..7 stay zero)
+    double *const wsm = wsm_all + wid * 32 * WSTR;
+    for (int t = lane; t < 32 * WSTR; t += 32) wsm[t] = 0.0;
+#else
+    (void)wsm_all;
+#endif
     __syncthreads();
-    for (int t = threadIdx.x; t < G * PMAX; t += blockDim.x) {
-        const int i = t / PMAX, a = t % PMAX;
-        double m = 0.0;
-        for (int b = 0; b <= a && b < p; ++b) m = fma(Li[i * PMAX * PMAX + a * PMAX + b], comp[i].mu[b], m);
-        mL[t] = m;
-    }
+    for (int t = threadIdx.x; t < G * PMAX; t += blockDim.x)
+        t_linv_col(comp[t / PMAX], p, t % PMAX, Li + (t / PMAX) * PMAX * PMAX);
+    __syncthreads();
+    for (int t = threadIdx.x; t < G * PMAX; t += blockDim.x)
+        mL[t] = t_ml_row(comp[t / PMAX], p, t % PMAX, Li + (t / PMAX) * PMAX * PMAX);
     __syncthreads();
     const bool nrm = A.family == 1;
-    double s0[G], s1[G], s7[G], s2[G], c0[G], c1[G];
+    double s0[G], s1[G], s7[G], c0[G], c1[G];
 #pragma unroll
-    for (int i = 0; i < G; ++i) s0[i] = s1[i] = s7[i] = s2[i] = c0[i] = c1[i] = 0.0;
+    for (int i = 0; i < G; ++i) s0[i] = s1[i] = s7[i] = c0[i] = c1[i] = 0.0;
+#if CFUST_T_P2 == 2
+    double c20 = 0.0, c21 = 0.0;   // S2 of component cm, coordinates 2 ck, 2 ck + 1 (DMMA fragment)
+#else
+    double s2[G];
+#pragma unroll
+    for (int i = 0; i < G; ++i) s2[i] = 0.0;
+#endif
     double ll = 0.0;
     const int cm = lane >> 2, ck = lane & 3;
     const int64_t n = A.n;
     const int64_t ntiles = (n + 31) / 32;
-    for (int64_t tile = int64_t(blockIdx.x) * TW + wid; tile < ntiles; tile += int64_t(gridDim.x) * TW) {
+    const int64_t tstride = int64_t(gridDim.x) * TW;
+#if CFUST_T_TMA
+    double *const yw = ybuf + wid * 2 * 32 * PMAX;
+    uint64_t *const mw = mbar + 2 * wid;
+    const uint32_t tbytes = uint32_t(32 * p * sizeof(double));   // a full tile: 256 p bytes (16 | 256 p)
+    // bulk copy of tile t (if it is a full one; the ragged last tile is copied by the lanes) into buffer b
+    auto issue = [&](int64_t t, int b) {
+        if (lane == 0 && t < ntiles && (t + 1) * 32 <= n) {
+            fence_proxy_async();   // this warp's earlier generic reads of buffer b precede the async write
+            mbar_expect_tx(mw + b, tbytes);
+            bulk_g2s(yw + b * 32 * PMAX, A.y + t * 32 * p, tbytes, mw + b);
+        }
+    };
+    issue(int64_t(blockIdx.x) * TW + wid, 0);
+    int kk = 0;
+#endif
+    for (int64_t tile = int64_t(blockIdx.x) * TW + wid; tile < ntiles; tile += tstride) {
         const int64_t j = tile * 32 + lane;
         const bool valid = j < n;
         double y[PMAX];
+#if CFUST_T_TMA
+        const int buf = kk & 1;
+        __syncwarp();   // every lane is done with buffer buf ^ 1 (the previous tile)
+        issue(tile + tstride, buf ^ 1);
+        double *const ys = yw + buf * 32 * PMAX;
+        if ((tile + 1) * 32 <= n) {
+            mbar_wait(mw + buf, (kk >> 1) & 1);
+        } else {   // ragged last tile: rows past n are zero
+            for (int a = 0; a < p; ++a) ys[lane * p + a] = valid ? A.y[j * p + a] : 0.0;
+            __syncwarp();
+        }
+        ++kk;
+        if (p == PMAX) {
+#pragma unroll
+            for (int a = 0; a < PMAX; a += 2) {
+                const double2 v2 = *reinterpret_cast<const double2 *>(ys + lane * PMAX + a);
+                y[a] = v2.x;
+                y[a + 1] = v2.y;
+            }
+        } else {
+#pragma unroll
+            for (int a = 0; a < PMAX; ++a) y[a] = (a < p) ? ys[lane * p + a] : 0.0;
+        }
+#else
+#if CFUST_T_P2 == 2
+        __syncwarp();   // every lane is done reading the previous tile's w rows
+#endif
         if (p == PMAX) {   // 64-byte rows: four 16-byte loads per lane
 #pragma unroll
             for (int a = 0; a < PMAX; a += 2) {
@@ -1065,6 +1146,7 @@ __global__ void __launch_bounds__(TW * 32, CFUST_T_MB) estep_t_mma_kernel(EArgs 
 #pragma unroll
             for (int a = 0; a < PMAX; ++a) y[a] = (valid && a < p) ? __ldg(A.y + j * p + a) : 0.0;
         }
+#endif
         double lf[G], dd[G], l1[G];
         double mx = -CUDART_INF;
 #pragma unroll
@@ -1118,16 +1200,33 @@ __global__ void __launch_bounds__(TW * 32, CFUST_T_MB) estep_t_mma_kernel(EArgs 
             s7[i] = fma(tau, e1me2, s7[i]);
         }
         // phase 2: 8 groups of 4 observations
+#if CFUST_T_P2 == 2
+#pragma unroll
+        for (int i = 0; i < G; ++i) wsm[lane * WSTR + i] = w[i];
+        __syncwarp();
+#endif
 #pragma unroll 2
         for (int sg = 0; sg < 8; ++sg) {
+#if CFUST_T_TMA
+            const double yv = (cm < p) ? ys[(4 * sg + ck) * p + cm] : 0.0;
+#else
             const int64_t jj = tile * 32 + 4 * sg + ck;
             const double yv = (cm < p && jj < n) ? __ldg(A.y + jj * p + cm) : 0.0;
+#endif
+#if CFUST_T_P2 == 2
+            // S2 of every component in one DMMA: A(m = component, k) = w_{4sg+k, m}, B(k, n) = y_{4sg+k, n}
+            const double *wq = wsm + (4 * sg + ck) * WSTR;
+            dmma_884(c20, c21, wq[cm], yv);
+#pragma unroll
+            for (int i = 0; i < G; ++i) dmma_884(c0[i], c1[i], wq[i] * yv, yv);
+#else
 #pragma unroll
             for (int i = 0; i < G; ++i) {
                 const double a = __shfl_sync(0xffffffffu, w[i], 4 * sg + ck) * yv;
                 s2[i] += a;
                 dmma_884(c0[i], c1[i], a, yv);
             }
+#endif
         }
     }
     // ---- warp epilogue -> red[wid][*], then block sum over warps in fixed order
@@ -1139,12 +1238,19 @@ __global__ void __launch_bounds__(TW * 32, CFUST_T_MB) estep_t_mma_kernel(EArgs 
 #pragma unroll
         for (int i = 0; i < G; ++i) {
             const double t0 = warp_sum(s0[i]), t1 = warp_sum(s1[i]), t7 = warp_sum(s7[i]);
+            double *ri = rw + i * K;
+            if (lane == 0) { ri[0] = t0; ri[1] = t1; ri[K - 1] = t7; }
+#if CFUST_T_P2 == 2
+            if (cm == i) {
+                if (2 * ck < p) ri[2 + 2 * ck] = c20;
+                if (2 * ck + 1 < p) ri[2 + 2 * ck + 1] = c21;
+            }
+#else
             double a2 = s2[i];
             a2 += __shfl_xor_sync(0xffffffffu, a2, 1);
             a2 += __shfl_xor_sync(0xffffffffu, a2, 2);
-            double *ri = rw + i * K;
-            if (lane == 0) { ri[0] = t0; ri[1] = t1; ri[K - 1] = t7; }
             if (ck == 0 && cm < p) ri[2 + cm] = a2;
+#endif
             // S3 upper, row-major packed: entry (a, b), a <= b
             const int a = cm;
 #pragma unroll
@@ -1821,7 +1927,9 @@ template <int G>
 static int launch_t_mma_g(const DevState &s, EArgs &a, int mode, cudaStream_t st, int *nb) {
     auto kern = estep_t_mma_kernel<G>;
     const size_t sm = sizeof(CompDev) * G + sizeof(double) * TW * (size_t(G) * s.K + 1)
-                      + sizeof(double) * G * (PMAX * PMAX + PMAX);   // L^{-1}, m
+                      + sizeof(double) * G * (PMAX * PMAX + PMAX)    // L^{-1}, m
+                      + 128 + (CFUST_T_TMA ? sizeof(double) * TW * 2 * 32 * PMAX + sizeof(uint64_t) * TW * 2 : 0)   // y tiles, mbarriers
+                      + (CFUST_T_P2 == 2 ? sizeof(double) * TW * 32 * WSTR : 0);   // w rows
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
     if (e != cudaSuccess) return int(e);
     int per_sm = 0;
