@@ -206,7 +206,8 @@ int cfust_nccl_unique_id(void *out);
 /* Diagnostic: evaluate a device special function element-wise on host arrays x[n] -> y[n]
  * (the exact code the kernels inline).  which: 0 Phi, 1 Phi^{-1}, 2 exp (x <= 0), 3 log
  * (0 < x <= 1), 4 univariate t CDF with df = aux, 5 chi-square quantile with df = aux,
- * 6 digamma, 7 sqrt, 8 trigamma (the M-step's nu Newton step).  No context needed; CFUST_ECUDA
+ * 6 digamma, 7 sqrt, 8 trigamma (the M-step's nu Newton step), 9 log Gamma (x > 0, the M-step's
+ * derived constants).  No context needed; CFUST_ECUDA
  * without a device. */
 int cfust_eval_special(int32_t which, const double *x, double *y, int64_t n, double aux);
 

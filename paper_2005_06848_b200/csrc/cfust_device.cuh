@@ -54,25 +54,77 @@ __device__ __forceinline__ double lattice_w(const LatticeDev& L, int l, int k) {
 __device__ __forceinline__ double Phi(double x) { return Phi_fast(x); }
 __device__ __forceinline__ double Phiinv(double u) { return Phiinv_fast(u); }
 
-// digamma: upward recurrence to x >= 16, then the Stirling-type asymptotic series.  The
-// recurrence sum  sum_k 1/(x+k)  is accumulated as one fraction num/den (two FMAs per step, one
-// division) — the nu bisection of the M-step calls this ~50 times per component on one thread.
+// digamma and trigamma for x > 0: upward recurrence to x >= 10, then the Stirling-type asymptotic
+// series through the B_16 (digamma) / B_18 (trigamma) terms (truncation < 1e-17 relative at x = 10).
+// The recurrence sums  sum_k 1/(x+k)  and  sum_k 1/(x+k)^2  are accumulated as fractions num/den,
+// two steps per iteration (1/x + 1/(x+1) = (2x+1)/(x(x+1))), which halves the dependent chain of the
+// M-step's nu root (one serial Newton chain per component, tests/test_gpu_special.py for accuracy).
+__device__ __forceinline__ double digamma_asym(double x) {   // x >= 10
+    const double r = div_fast(1.0, x), r2 = r * r;
+    const double ser = r2 * (1.0 / 12 - r2 * (1.0 / 120 - r2 * (1.0 / 252 - r2 * (1.0 / 240 - r2 * (1.0 / 132
+                      - r2 * (691.0 / 32760 - r2 * (1.0 / 12 - r2 * (3617.0 / 8160))))))));
+    return log_unit(x) - 0.5 * r - ser;
+}
+__device__ __forceinline__ double trigamma_asym(double x) {   // x >= 10
+    const double r = div_fast(1.0, x), r2 = r * r;
+    return r * (1.0 + r * (0.5 + r * (1.0 / 6 - r2 * (1.0 / 30 - r2 * (1.0 / 42 - r2 * (1.0 / 30 - r2 * (5.0 / 66
+           - r2 * (691.0 / 2730 - r2 * (7.0 / 6 - r2 * (3617.0 / 510 - r2 * (43867.0 / 798)))))))))));
+}
 __device__ inline double dev_digamma(double x) {
     double num = 0.0, den = 1.0;
-    while (x < 16.0) { num = fma(num, x, den); den *= x; x += 1.0; }   // num/den += 1/x
-    const double r = div_fast(1.0, x), r2 = r * r;
-    const double ser = r2 * (1.0 / 12 - r2 * (1.0 / 120 - r2 * (1.0 / 252 - r2 * (1.0 / 240 - r2 * (1.0 / 132)))));
-    return log(x) - 0.5 * r - ser - div_fast(num, den);
+    while (x < 9.0) {   // num/den += 1/x + 1/(x+1)
+        const double t = x * (x + 1.0);
+        num = fma(num, t, den * fma(2.0, x, 1.0));
+        den *= t;
+        x += 2.0;
+    }
+    if (x < 10.0) { num = fma(num, x, den); den *= x; x += 1.0; }
+    return digamma_asym(x) - div_fast(num, den);
 }
-
-// trigamma psi'(x), x > 0: recurrence sum 1/(x+k)^2 to x >= 16, then the asymptotic series
-// 1/x + 1/(2x^2) + 1/(6x^3) - 1/(30x^5) + 1/(42x^7) - 1/(30x^9) + 5/(66x^11) (error < 1e-15 there).
 __device__ inline double dev_trigamma(double x) {
     double num = 0.0, den = 1.0;
-    while (x < 16.0) { const double x2 = x * x; num = fma(num, x2, den); den *= x2; x += 1.0; }   // num/den += 1/x^2
+    while (x < 9.0) {   // num/den += 1/x^2 + 1/(x+1)^2
+        const double x2 = x * x, x12 = (x + 1.0) * (x + 1.0), t = x2 * x12;
+        num = fma(num, t, den * (x2 + x12));
+        den *= t;
+        x += 2.0;
+    }
+    if (x < 10.0) { const double x2 = x * x; num = fma(num, x2, den); den *= x2; x += 1.0; }
+    return div_fast(num, den) + trigamma_asym(x);
+}
+// both at once (the nu Newton step needs psi and psi'): the two recurrences interleave
+__device__ inline void dev_psi01(double x, double &psi, double &psi1) {
+    double nd = 0.0, dd = 1.0, nt = 0.0, dt = 1.0;
+    while (x < 9.0) {
+        const double t = x * (x + 1.0), x2 = x * x, x12 = (x + 1.0) * (x + 1.0), u = x2 * x12;
+        nd = fma(nd, t, dd * fma(2.0, x, 1.0));
+        dd *= t;
+        nt = fma(nt, u, dt * (x2 + x12));
+        dt *= u;
+        x += 2.0;
+    }
+    if (x < 10.0) {
+        nd = fma(nd, x, dd); dd *= x;
+        const double x2 = x * x;
+        nt = fma(nt, x2, dt); dt *= x2;
+        x += 1.0;
+    }
+    psi = digamma_asym(x) - div_fast(nd, dd);
+    psi1 = div_fast(nt, dt) + trigamma_asym(x);
+}
+
+// log Gamma(x), x > 0 (the M-step's derived constants): upward recurrence to y = x + n >= 10 as one
+// product, then Stirling's series through the B_16 term (truncation < 4e-17 at y = 10):
+//   lgamma(x) = (y - 1/2) log y - y + log(2 pi)/2 + sum_k B_2k / (2k (2k-1) y^(2k-1)) - log(x (x+1) ... (x+n-1)).
+// One code path for every argument (libdevice lgamma branches by range: lanes with different ranges
+// run one after another); absolute error ~1e-15 (tests/test_gpu_special.py).
+__device__ inline double dev_lgamma_pos(double x) {
+    double prod = 1.0;
+    while (x < 10.0) { prod *= x; x += 1.0; }
     const double r = div_fast(1.0, x), r2 = r * r;
-    const double ser = r * (1.0 + r * (0.5 + r * (1.0 / 6 - r2 * (1.0 / 30 - r2 * (1.0 / 42 - r2 * (1.0 / 30 - r2 * (5.0 / 66)))))));
-    return div_fast(num, den) + ser;
+    const double ser = r * (1.0 / 12 - r2 * (1.0 / 360 - r2 * (1.0 / 1260 - r2 * (1.0 / 1680 - r2 * (1.0 / 1188
+                       - r2 * (691.0 / 360360 - r2 * (1.0 / 156 - r2 * (3617.0 / 122400))))))));
+    return fma(x - 0.5, log_unit(x), 0.91893853320467274178 - x) + ser - log_unit(prod);
 }
 
 // Continued fractions by the fundamental (Wallis) recurrences

@@ -1372,7 +1372,6 @@ __device__ inline void chol_solve_dev(int n, const double *L, int ldl, double *x
 
 
 
-__device__ inline double nu_equation(double nu, double c) { return log(0.5 * nu) - dev_digamma(0.5 * nu) + 1.0 + c; }
 
 
 // ------------------------------------------------------------------------------------------
@@ -1380,26 +1379,35 @@ __device__ inline double nu_equation(double nu, double c) { return log(0.5 * nu)
 // component, one warp per component: every matrix entry is computed by one lane
 // in the plain left-to-right operation order; only independent entries run in parallel.
 
-// Cholesky of the n x n matrix A (row stride lda) into L (stride ldl), column by column: lane 0 the
-// pivot, lanes i > j the column below it.  false (in all lanes) if a pivot is <= 1e-300.
-__device__ bool warp_chol(int n, const double *A, int lda, double *L, int ldl, int lane, int *okflag) {
-    for (int j = 0; j < n; ++j) {
-        if (lane == 0) {
-            double d = A[j * lda + j];
-            for (int k = 0; k < j; ++k) d -= L[j * ldl + k] * L[j * ldl + k];
-            *okflag = (d > 1e-300);
-            L[j * ldl + j] = *okflag ? sqrt_fast(d) : 0.0;   // rsqrt + Newton: no IEEE slow path
-        }
-        __syncwarp();
-        if (!*okflag) return false;
-        for (int i = j + 1 + lane; i < n; i += 32) {
-            double v = A[i * lda + j];
-            for (int k = 0; k < j; ++k) v -= L[i * ldl + k] * L[j * ldl + k];
-            L[i * ldl + j] = div_fast(v, L[j * ldl + j]);
-        }
-        __syncwarp();
+// Cholesky of the n x n matrix A (row stride lda, n <= PMAX) into L (stride ldl; the lower triangle
+// incl. the diagonal is written), left-looking column by column with row a of L in lane a's registers:
+// column j takes L[j][0..j-1] from lane j by shuffles, pivot d = A_jj - sum_k L_jk^2 and
+// L_aj = (A_aj - sum_k L_ak L_jk) / L_jj in ascending k.  false (in all lanes) if a pivot is <= 1e-300.
+// (Round 1 staged the columns through shared memory with lane 0 computing each pivot: ~5x the latency.)
+__device__ bool warp_chol(int n, const double *A, int lda, double *L, int ldl, int lane) {
+    double r[PMAX];
+#pragma unroll
+    for (int k = 0; k < PMAX; ++k) r[k] = (lane < n && k < n) ? A[lane * lda + k] : 0.0;
+    bool ok = true;
+#pragma unroll
+    for (int j = 0; j < PMAX; ++j) {
+        if (j >= n) break;
+        double v = r[j];
+#pragma unroll
+        for (int k = 0; k < j; ++k) v -= r[k] * __shfl_sync(0xffffffffu, r[k], j);
+        const double d = __shfl_sync(0xffffffffu, v, j);
+        if (!(d > 1e-300)) { ok = false; break; }
+        const double ljj = sqrt_fast(d);   // rsqrt + Newton: no IEEE slow path
+        if (lane == j) r[j] = ljj;
+        else if (lane > j) r[j] = div_fast(v, ljj);
     }
-    return true;
+    if (ok && lane < n) {
+#pragma unroll
+        for (int k = 0; k < PMAX; ++k)
+            if (k <= lane) L[lane * ldl + k] = r[k];
+    }
+    __syncwarp();
+    return ok;
 }
 
 constexpr int KMAX = 2 + PMAX + PMAX * (PMAX + 1) / 2 + QMAX + QMAX * (QMAX + 1) / 2 + PMAX * QMAX + 1;
@@ -1411,28 +1419,46 @@ struct MsWork {
     int ok;
 };
 
+// CFUST_MSTEP_PROF (experiment builds): clock64 stamps per warp of mstep_fused_kernel, printed at exit
+#ifndef CFUST_MSTEP_PROF
+#define CFUST_MSTEP_PROF 0
+#endif
+#if CFUST_MSTEP_PROF
+__device__ long long g_mprof[2 * GMAX][24];
+#define MPROF(k) do { if ((threadIdx.x & 31) == 0) g_mprof[threadIdx.x >> 5][k] = clock64(); } while (0)
+#else
+#define MPROF(k) do { } while (0)
+#endif
+
 __device__ double nu_update(const DevState &s, int i, double S0, double S7) {
     const double cst = S7 / S0;
     // nu: root of g(nu) = log(nu/2) - psi(nu/2) + 1 + S7/S0 on [nu_lo, nu_hi] (reading A7; g decreasing,
     // clamped when there is no sign change): safeguarded Newton from the previous nu, the bracket kept and
     // bisection taken whenever a step leaves it, to |dnu| <= 1e-13 nu (the oracle bisects to 1e-12: both
-    // land within that tolerance of the root).
-    double nu;
-    if (nu_equation(s.nu_hi, cst) > 0.0) nu = s.nu_hi;
-    else if (nu_equation(s.nu_lo, cst) < 0.0) nu = s.nu_lo;
-    else {
-        double lo = s.nu_lo, hi = s.nu_hi;
-        nu = fmin(fmax(s.nu[i], lo), hi);
-        for (int it = 0; it < 200; ++it) {
-            const double gv = nu_equation(nu, cst);
-            if (gv > 0.0) lo = nu; else hi = nu;
-            const double dg = div_fast(1.0, nu) - 0.5 * dev_trigamma(0.5 * nu);
-            double nn = nu - div_fast(gv, dg);
-            if (!(nn > lo && nn < hi)) nn = 0.5 * (lo + hi);
-            const bool done = fabs(nn - nu) <= 1e-13 * nu || hi - lo <= 1e-13 * nu;
-            nu = nn;
-            if (done) break;
-        }
+    // land within that tolerance of the root).  Called by a whole warp: lanes 0, 1, 2 evaluate g at
+    // nu_hi, nu_lo and the starting point at once (one pass of the same code), then every lane runs
+    // the same Newton chain (psi and psi' from one interleaved recurrence).
+    const int lane = threadIdx.x & 31;
+    const double lo0 = s.nu_lo, hi0 = s.nu_hi, start = fmin(fmax(s.nu[i], lo0), hi0);
+    const double x0 = (lane == 0) ? hi0 : (lane == 1) ? lo0 : start;
+    double ps, ps1;
+    dev_psi01(0.5 * x0, ps, ps1);
+    const double g0 = log_unit(0.5 * x0) - ps + 1.0 + cst;
+    const double ghi = __shfl_sync(0xffffffffu, g0, 0), glo = __shfl_sync(0xffffffffu, g0, 1);
+    double gv = __shfl_sync(0xffffffffu, g0, 2), psi1 = __shfl_sync(0xffffffffu, ps1, 2);
+    if (ghi > 0.0) return hi0;
+    if (glo < 0.0) return lo0;
+    double lo = lo0, hi = hi0, nu = start;
+    for (int it = 0; it < 200; ++it) {
+        if (gv > 0.0) lo = nu; else hi = nu;
+        const double dg = div_fast(1.0, nu) - 0.5 * psi1;
+        double nn = nu - div_fast(gv, dg);
+        if (!(nn > lo && nn < hi)) nn = 0.5 * (lo + hi);
+        const bool done = fabs(nn - nu) <= 1e-13 * nu || hi - lo <= 1e-13 * nu;
+        nu = nn;
+        if (done) break;
+        dev_psi01(0.5 * nu, ps, psi1);
+        gv = log_unit(0.5 * nu) - ps + 1.0 + cst;
     }
     return nu;
 }
@@ -1441,6 +1467,7 @@ __device__ int mstep_warp(const DevState &s, int i, MsWork &w, int lane, bool do
     const int p = s.p, q = s.q, K = s.K;
     for (int e = lane; e < K; e += 32) w.Sv[e] = s.stats[size_t(i) * K + e];
     __syncwarp();
+    MPROF(2);
     const double *S = w.Sv;
     const double S0 = S[0], S1 = S[1];
     const double *S2 = S + 2, *S3p = S2 + p, *S4 = S3p + p * (p + 1) / 2, *S5p = S4 + q;
@@ -1461,6 +1488,7 @@ __device__ int mstep_warp(const DevState &s, int i, MsWork &w, int lane, bool do
     }
     for (int t = lane; t < p * q; t += 32) w.D[t] = s.delta[size_t(i) * p * q + t];
     __syncwarp();
+    MPROF(3);
     for (int a = lane; a < p; a += 32) {
         double v = S2[a];
         for (int k = 0; k < q; ++k) v -= w.D[a * q + k] * S4[k];
@@ -1473,7 +1501,7 @@ __device__ int mstep_warp(const DevState &s, int i, MsWork &w, int lane, bool do
     }
     __syncwarp();
     if (q > 0) {
-        if (!warp_chol(q, w.S5, QMAX, w.L5, QMAX, lane, &w.ok)) return -4;
+        if (!warp_chol(q, w.S5, QMAX, w.L5, QMAX, lane)) return -4;
         for (int a = lane; a < p; a += 32) {   // row a of B S5^{-1}
             double x[QMAX];
             for (int k = 0; k < q; ++k) x[k] = w.B[a * QMAX + k];
@@ -1482,6 +1510,7 @@ __device__ int mstep_warp(const DevState &s, int i, MsWork &w, int lane, bool do
         }
         __syncwarp();
     }
+    MPROF(4);
     for (int t = lane; t < p * p; t += 32) {
         const int a = t / p, b = t % p;
         double v = w.S3[a * PMAX + b] - S2[a] * w.mu[b] - w.mu[a] * S2[b] + S1 * w.mu[a] * w.mu[b];
@@ -1502,7 +1531,8 @@ __device__ int mstep_warp(const DevState &s, int i, MsWork &w, int lane, bool do
         if (a != b) w.Sg[a * p + b] = sym[c];
     }
     __syncwarp();
-    if (!warp_chol(p, w.Sg, p, w.Lt, PMAX, lane, &w.ok)) {   // ridge repair
+    MPROF(5);
+    if (!warp_chol(p, w.Sg, p, w.Lt, PMAX, lane)) {   // ridge repair
         if (lane == 0) {
             double md = 0.0;
             for (int a = 0; a < p; ++a) md += w.Sg[a * p + a];
@@ -1511,10 +1541,12 @@ __device__ int mstep_warp(const DevState &s, int i, MsWork &w, int lane, bool do
         __syncwarp();
         for (int a = lane; a < p; a += 32) w.Sg[a * p + a] += 1e-8 * w.md;
         __syncwarp();
-        if (!warp_chol(p, w.Sg, p, w.Lt, PMAX, lane, &w.ok)) return -4;
+        if (!warp_chol(p, w.Sg, p, w.Lt, PMAX, lane)) return -4;
     }
-    if (s.family == 1 || lane != 0 || !do_nu) return 0;   // skew-normal / Gaussian: no nu
-    w.nu = nu_update(s, i, S0, S7);
+    MPROF(6);
+    if (s.family == 1 || !do_nu) return 0;   // skew-normal / Gaussian: no nu
+    const double nu = nu_update(s, i, S0, S7);   // whole warp
+    if (lane == 0) w.nu = nu;
     return 0;
 }
 
@@ -1535,16 +1567,29 @@ struct DvWork {
     int ok;
 };
 
-__device__ int derive_warp(const DevState &s, int i, DvWork &w, CompDev &cd_out, int lane) {
+// Derived quantities of component i, one warp, in two parts so that the fused
+// M-step can run the matrix part while the nu root is still being solved:
+//   derive_matrices  chol Sigma (unless supplied), Omega = Sigma + Delta Delta', its factor L, 1/L_aa,
+//                    A = Delta' Omega^{-1}, Lambda = I - A Delta (symmetrised), log|Omega|, mu;
+//   derive_constants the nu- and pi-dependent constants (kappa, log pi, psi(m0/2), the t_1 lgamma
+//                    differences, log B(m/2, 1/2), 1/nu, log(nu/2)), then the CompDev copy-out.
+// inputs_ready: w.Sg, w.D, w.cd.mu and w.Lc = chol(Sigma) already hold this component's values (the
+// fused M-step supplies its own results — the same bits derive would read back and recompute).
+__device__ int derive_matrices(const DevState &s, int i, DvWork &w, int lane, bool inputs_ready = false) {
     const int p = s.p, q = s.q;
     CompDev &cd = w.cd;
-    for (int t = lane; t < p * p; t += 32) w.Sg[t] = s.sigma[size_t(i) * p * p + t];
-    for (int t = lane; t < p * q; t += 32) w.D[t] = s.delta[size_t(i) * p * q + t];
+    if (!inputs_ready) {
+        for (int t = lane; t < p * p; t += 32) w.Sg[t] = s.sigma[size_t(i) * p * p + t];
+        for (int t = lane; t < p * q; t += 32) w.D[t] = s.delta[size_t(i) * p * q + t];
+        for (int a = lane; a < p; a += 32) cd.mu[a] = s.mu[size_t(i) * p + a];
+    }
     for (int t = lane; t < PMAX * PMAX; t += 32) { cd.L[t] = 0.0; w.Om[t] = 0.0; }
     for (int t = lane; t < QMAX * PMAX; t += 32) cd.A[t] = 0.0;
     for (int t = lane; t < QMAX * QMAX; t += 32) cd.Lam[t] = 0.0;
     __syncwarp();
-    if (!warp_chol(p, w.Sg, p, w.Lc, PMAX, lane, &w.ok)) return -4;   // Sigma itself must be PD
+    MPROF(10);
+    if (!inputs_ready && !warp_chol(p, w.Sg, p, w.Lc, PMAX, lane)) return -4;   // Sigma must be PD
+    MPROF(11);
     for (int t = lane; t < p * p; t += 32) {
         const int a = t / p, b = t % p;
         double v = w.Sg[a * p + b];
@@ -1558,29 +1603,21 @@ __device__ int derive_warp(const DevState &s, int i, DvWork &w, CompDev &cd_out,
             cd.L[t] = (a < p && b <= a) ? w.Lc[t] : 0.0;
         }
         __syncwarp();
-    } else if (!warp_chol(p, w.Om, PMAX, cd.L, PMAX, lane, &w.ok)) {
+    } else if (!warp_chol(p, w.Om, PMAX, cd.L, PMAX, lane)) {
         return -4;
     }
+    MPROF(12);
     for (int a = lane; a < PMAX; a += 32) cd.Linv[a] = (a < p) ? 1.0 / cd.L[a * PMAX + a] : 0.0;
-    for (int a = lane; a < p; a += 32) cd.mu[a] = s.mu[size_t(i) * p + a];
     for (int k = lane; k < q; k += 32) {   // A = Delta' Omega^{-1}: one column of Omega^{-1} Delta per lane
         double x[PMAX];
         for (int a = 0; a < p; ++a) x[a] = w.D[a * q + k];
         chol_solve_dev(p, cd.L, PMAX, x);
         for (int a = 0; a < p; ++a) cd.A[k * PMAX + a] = x[a];
     }
-    const double nu = s.nu[i], m0 = nu + p;
-    if (lane < 8) {   // the transcendental constants in parallel
-        double v = 0.0;
-        if (lane == 0) v = lgamma(0.5 * m0) - lgamma(0.5 * nu);
-        else if (lane == 1) v = lgamma(0.5 * (m0 + 1.0)) - lgamma(0.5 * m0);
-        else if (lane == 2) v = lgamma(0.5 * m0) - lgamma(0.5 * (m0 - 1.0));
-        else if (lane == 3) v = dev_digamma(0.5 * m0);
-        else if (lane >= 5) v = dev_t_lbeta(m0 + double(lane - 5));   // log B(m/2, 1/2), m = m0, m0+1, m0+2
-        else
-            for (int a = 0; a < p; ++a) v += 2.0 * log(cd.L[a * PMAX + a]);
-        w.lg[lane] = v;
-    }
+    // log|Omega| = sum_a 2 log L_aa (lanes a in parallel, summed in ascending a)
+    const double lv = log_unit(lane < p ? cd.L[lane * PMAX + lane] : 1.0);
+    double logdet = 0.0;
+    for (int a = 0; a < p; ++a) logdet += 2.0 * __shfl_sync(0xffffffffu, lv, a);
     __syncwarp();
     for (int t = lane; t < q * q; t += 32) {
         const int k = t / q, l = t % q;
@@ -1599,24 +1636,57 @@ __device__ int derive_warp(const DevState &s, int i, DvWork &w, CompDev &cd_out,
         const int k = t / q, l = t % q;
         if (k != l) cd.Lam[k * QMAX + l] = sym[c];
     }
+    if (lane == 0) w.lg[4] = logdet;
+    __syncwarp();
+    MPROF(13);
+    return 0;
+}
+
+// nu = nu_i and pi = pi_i of the committed parameters; every lane on ONE code path (divergent
+// branches would run one after another): lanes 0..5 lgamma at nu/2, (m0-1)/2, m0/2, (m0+1)/2,
+// (m0+2)/2, (m0+3)/2; lanes 0, 1, 2 log pi_i, log(nu pi) (Gaussian family: log 2 pi), log(nu/2).
+__device__ void derive_constants(const DevState &s, DvWork &w, double nu, double pii, CompDev &cd_out, int lane) {
+    const int p = s.p;
+    CompDev &cd = w.cd;
+    const double m0 = nu + p;
+    const double garg = (lane == 0) ? 0.5 * nu : 0.5 * (m0 + double(lane - 2));
+    const double lgv = dev_lgamma_pos(lane < 6 ? garg : 1.0);
+    MPROF(19);
+    const double larg = (lane == 0) ? pii : (lane == 1) ? ((s.family == 1) ? 2.0 * CUDART_PI : nu * CUDART_PI)
+                      : (lane == 2) ? 0.5 * nu : 1.0;
+    const double lv = log_unit(larg);
+    const double psi_m0 = dev_digamma(0.5 * m0);   // same argument in every lane: one pass
+    MPROF(21);
+    double G[6];
+#pragma unroll
+    for (int k = 0; k < 6; ++k) G[k] = __shfl_sync(0xffffffffu, lgv, k);
+    const double log_pi = __shfl_sync(0xffffffffu, lv, 0), log_nupi = __shfl_sync(0xffffffffu, lv, 1),
+                 log_hnu = __shfl_sync(0xffffffffu, lv, 2);
     if (lane == 0) {
         const double logdet = w.lg[4];
         cd.nu = nu;
         cd.m0 = m0;
-        cd.kappa = (s.family == 1) ? -0.5 * p * log(2.0 * CUDART_PI) - 0.5 * logdet   // log phi_p normaliser
-                                   : w.lg[0] - 0.5 * p * log(nu * CUDART_PI) - 0.5 * logdet;
-        cd.logpi = log(s.pi[i]);
-        cd.psi_half_m0 = w.lg[3];
-        cd.lgc_m0 = w.lg[1];
-        cd.lgc_m0m1 = w.lg[2];
-        for (int k = 0; k < 3; ++k) cd.lbt[k] = w.lg[5 + k];
-        cd.inv_nu = 1.0 / nu;
-        cd.log_half_nu = log(0.5 * nu);
+        cd.kappa = (s.family == 1) ? -0.5 * p * log_nupi - 0.5 * logdet   // log phi_p normaliser (log 2 pi)
+                                   : (G[2] - G[0]) - 0.5 * p * log_nupi - 0.5 * logdet;
+        cd.logpi = log_pi;
+        cd.psi_half_m0 = psi_m0;
+        cd.lgc_m0 = G[3] - G[2];     // lgamma((m0+1)/2) - lgamma(m0/2)
+        cd.lgc_m0m1 = G[2] - G[1];   // lgamma(m0/2) - lgamma((m0-1)/2)
+        for (int k = 0; k < 3; ++k) cd.lbt[k] = G[2 + k] + 0.5723649429247001 - G[3 + k];   // log B(m/2, 1/2), m = m0 + k
+        cd.inv_nu = div_fast(1.0, nu);
+        cd.log_half_nu = log_hnu;
     }
     __syncwarp();
+    MPROF(14);
     double *dst = reinterpret_cast<double *>(&cd_out);
     const double *src = reinterpret_cast<const double *>(&cd);
     for (int t = lane; t < int(sizeof(CompDev) / sizeof(double)); t += 32) dst[t] = src[t];
+}
+
+__device__ int derive_warp(const DevState &s, int i, DvWork &w, CompDev &cd_out, int lane) {
+    const int rc = derive_matrices(s, i, w, lane);
+    if (rc != 0) return rc;
+    derive_constants(s, w, s.nu[i], s.pi[i], cd_out, lane);
     return 0;
 }
 
@@ -1666,10 +1736,11 @@ union MsDvWork {
 // index at which the first error was seen (-1: none), [2] its kind (1 E-step, 2 M-step / derive).
 __global__ void __launch_bounds__(64 * GMAX) mstep_fused_kernel(DevState s) {
     __shared__ MsDvWork w[GMAX];
-    __shared__ double nu_new[GMAX];
+    __shared__ double nu_new[GMAX], s0sh[GMAX];
     __shared__ int gate, slot;
     const int i = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int GK = s.g * s.K;
+    MPROF(0);
     if (threadIdx.x == 0) {
         // l^(k) of the E-step that produced these statistics -> trace slot (cfust_fit, no host sync)
         int j = -1;
@@ -1690,43 +1761,92 @@ __global__ void __launch_bounds__(64 * GMAX) mstep_fused_kernel(DevState s) {
         gate = eflag || s.status[1] < 0;
     }
     __syncthreads();
+    MPROF(1);
     if (gate) return;
     const bool tnu = s.family != 1;   // skew-t: nu solved by warp g + i, concurrently with warp i's updates
+    // This component's M-step results travel to the commit in registers (MsWork and DvWork share
+    // storage, and nothing is committed before every component succeeded).
+    constexpr int R2 = (PMAX * PMAX + 31) / 32, RD = (PMAX * QMAX + 31) / 32;
+    double mur = 0.0, sgr[R2], dr[RD];
     if (i < s.g) {
-        const int rc = mstep_warp(s, i, w[i].ms, lane, false);
+        int rc = mstep_warp(s, i, w[i].ms, lane, false);
+        if (lane == 0) s0sh[i] = w[i].ms.Sv[0];
+        if (rc == 0) {
+            const int p = s.p, q = s.q;
+            double ltr[R2];
+            if (lane < p) mur = w[i].ms.mu[lane];
+#pragma unroll
+            for (int c = 0; c < R2; ++c) {
+                const int t = lane + 32 * c;
+                sgr[c] = (t < p * p) ? w[i].ms.Sg[t] : 0.0;
+                ltr[c] = w[i].ms.Lt[t];
+            }
+#pragma unroll
+            for (int c = 0; c < RD; ++c) dr[c] = (lane + 32 * c < p * q) ? w[i].ms.D[lane + 32 * c] : 0.0;
+            __syncwarp();
+            DvWork &dv = w[i].dv;
+            if (lane < p) dv.cd.mu[lane] = mur;
+#pragma unroll
+            for (int c = 0; c < R2; ++c) {
+                const int t = lane + 32 * c;
+                if (t < p * p) dv.Sg[t] = sgr[c];
+                dv.Lc[t] = ltr[c];   // chol of exactly this Sigma (ridge repair included)
+            }
+#pragma unroll
+            for (int c = 0; c < RD; ++c)
+                if (lane + 32 * c < p * q) dv.D[lane + 32 * c] = dr[c];
+            __syncwarp();
+            // the derived matrices (Omega, its factor, A, Lambda, log|Omega|) overlap the nu root
+            rc = derive_matrices(s, i, dv, lane, true);
+        }
         if (rc != 0 && lane == 0) atomicMin(s.status + 1, rc);
-    } else if (tnu && i < 2 * s.g && lane == 0) {
+        MPROF(16);
+    } else if (tnu && i < 2 * s.g) {
         const int c = i - s.g;
         const double S0 = s.stats[size_t(c) * s.K], S7 = s.stats[size_t(c) * s.K + s.K - 1];
-        if (S0 >= 1e-10) nu_new[c] = nu_update(s, c, S0, S7);   // (S0 < 1e-10: warp c reports -6)
+        if (S0 >= 1e-10) {   // (S0 < 1e-10: warp c reports -6)
+            const double nu = nu_update(s, c, S0, S7);   // whole warp
+            if (lane == 0) nu_new[c] = nu;
+        }
+        MPROF(7);
     }
     __syncthreads();
+    MPROF(8);
     if (reinterpret_cast<volatile int *>(s.status)[1] < 0) {   // some component failed: commit nothing
         if (threadIdx.x == 0 && s.fitctl && s.fitctl[1] < 0) { s.fitctl[1] = slot; s.fitctl[2] = 2; }
         return;
     }
     if (i >= s.g) return;
-    mstep_commit(s, i, w[i].ms, lane);
-    if (tnu && lane == 0) s.nu[i] = nu_new[i];
-    __syncwarp();   // the union's MsWork is dead from here on (derive reuses the storage)
-    if (lane == 0) {
-        double tot = 0.0, mine = 0.0;
-        for (int c = 0; c < s.g; ++c) {
-            double v = s.stats[size_t(c) * s.K] / s.n_total;
-            v = (v < 1e-10) ? 1e-10 : v;
-            tot += v;
-            if (c == i) mine = v;
-        }
-        s.pi[i] = mine / tot;
+    {   // commit mu, Sigma, Delta, nu of component i
+        const int p = s.p, q = s.q;
+        if (lane < p) s.mu[size_t(i) * p + lane] = mur;
+#pragma unroll
+        for (int c = 0; c < R2; ++c)
+            if (lane + 32 * c < p * p) s.sigma[size_t(i) * p * p + lane + 32 * c] = sgr[c];
+#pragma unroll
+        for (int c = 0; c < RD; ++c)
+            if (lane + 32 * c < p * q) s.delta[size_t(i) * p * q + lane + 32 * c] = dr[c];
     }
-    __syncwarp();
-    // derive cannot fail here except by rounding (Sigma just passed its Cholesky; Omega = Sigma +
-    // Delta Delta' is then PD): if it does, the error is returned and the caller re-initialises.
-    const int rc = derive_warp(s, i, w[i].dv, s.comp[i], lane);
-    if (rc != 0 && lane == 0) {
-        atomicMin(s.status + 1, rc);
-        if (s.fitctl) atomicCAS(s.fitctl + 2, 0, 2);
+    const double nu = tnu ? nu_new[i] : s.nu[i];
+    if (tnu && lane == 0) s.nu[i] = nu;
+    // pi <- S0 / n_total floored at 1e-10, renormalised (lanes c < g in parallel, summed in ascending c)
+    double v = (lane < s.g) ? s0sh[lane] / s.n_total : 0.0;
+    v = (v < 1e-10) ? 1e-10 : v;
+    double tot = 0.0;
+    for (int c = 0; c < s.g; ++c) tot += __shfl_sync(0xffffffffu, v, c);
+    const double pii = __shfl_sync(0xffffffffu, v, i) / tot;
+    if (lane == 0) s.pi[i] = pii;
+    MPROF(9);
+    derive_constants(s, w[i].dv, nu, pii, s.comp[i], lane);
+    MPROF(15);
+#if CFUST_MSTEP_PROF
+    if (lane == 0) {   // this (component) warp's stamps relative to its own start
+        const long long *t = g_mprof[i];
+        printf("MPROF comp %d: gate %lld stats %lld D %lld Sg %lld chol %lld dmat %lld nu %lld | bar %lld pi %lld lgam %lld cst %lld end %lld\n",
+               i, t[1] - t[0], t[2] - t[0], t[4] - t[0], t[5] - t[0], t[6] - t[0], t[16] - t[0], g_mprof[s.g + i][7] - t[0],
+               t[8] - t[0], t[9] - t[0], t[19] - t[0], t[21] - t[0], t[15] - t[0]);
     }
+#endif
 }
 
 __global__ void __launch_bounds__(32) derive_kernel(DevState s) {
@@ -1783,6 +1903,7 @@ __global__ void special_kernel(int which, const double *__restrict__ x, double *
             case 6: r = dev_digamma(v); break;
             case 7: r = sqrt_fast(v); break;
             case 8: r = dev_trigamma(v); break;
+            case 9: r = dev_lgamma_pos(v); break;
             default: r = CUDART_NAN;
         }
         y[t] = r;

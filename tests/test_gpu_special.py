@@ -78,6 +78,16 @@ def test_t_cdf_chi2_digamma(cf, df):
     assert np.max(np.abs(d - sp.digamma([0.05, 0.5, 1.0, 2.5, 10.0, 77.0, df]))) < 1e-13
 
 
+def test_lgamma_range(cf):
+    """log Gamma of the M-step's derived constants (one code path for every argument) vs scipy:
+    absolute 1e-14 where |lgamma| <= 1 (Stirling after the recurrence: ~1e-15 cancellation error),
+    relative 1e-14 elsewhere, over the df range (nu/2, (nu+p+k)/2)."""
+    x = np.concatenate([np.linspace(0.05, 40, 800), np.geomspace(40, 600, 50), [0.5, 1.0, 1.5, 2.0, 2.5, 10.0]])
+    got = cf.eval_special("lgamma", x)
+    ref = sp.gammaln(x)
+    assert np.max(np.abs(got - ref) / np.maximum(1.0, np.abs(ref))) < 1e-14
+
+
 def test_trigamma_and_digamma_range(cf):
     """psi and psi' (the M-step's nu equation and its Newton derivative) vs scipy over the nu range."""
     x = np.concatenate([np.linspace(0.05, 40, 800), [0.5, 1.0, 16.0, 100.0, 500.0]])
