@@ -370,6 +370,7 @@ void cfust_destroy(cfust_ctx *ctx) {
     cudaFree(s.comp);
     cudaFree(s.chi);
     cudaFree(s.W);
+    cudaFree(s.wperm);
     cudaFree(s.partials);
     cudaFree(s.stats);
     cudaFree(s.status);
@@ -467,6 +468,7 @@ int cfust_em_init(cfust_ctx **out, const double *y, int64_t n, int32_t p, int32_
                   alloc((void **)&s.nu, sizeof(double) * g) && alloc((void **)&s.comp, comp_dev_size() * g) &&
                   alloc((void **)&s.chi, sizeof(double) * g * CHI_ROWS * (M > 0 ? M : 1)) &&
                   alloc((void **)&s.W, sizeof(double) * nz * (M > 0 ? M : 1)) &&
+                  alloc((void **)&s.wperm, sizeof(int) * (M > 0 ? M : 1)) &&
                   alloc((void **)&s.partials, sizeof(double) * size_t(max_partial_blocks(s)) * GK1) &&
                   alloc((void **)&s.stats, sizeof(double) * (GK1 + 1)) && alloc((void **)&s.status, sizeof(int) * 4) &&
                   alloc((void **)&ctx->d_ll, sizeof(double) * 2) &&
@@ -506,7 +508,7 @@ int cfust_em_init(cfust_ctx **out, const double *y, int64_t n, int32_t p, int32_
             rc = fail(ctx, CFUST_ECUDA, cudaGetErrorString(cudaGetLastError()));
             break;
         }
-        ctx->launches += 4;
+        ctx->launches += 4 + (s.M > 0 ? 1 : 0);   // (+ the lattice sort for the chi nodes)
         // Multi-rank: the communicator is created BEFORE the validation verdict, and the status word
         // (non-finite y, derive errors) is max-reduced over ranks, so every rank returns the same
         // code — a rank failing alone would leave the others blocked in the next collective.

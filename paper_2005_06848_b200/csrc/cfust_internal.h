@@ -37,6 +37,7 @@ struct DevState {
     int split_force;                // warps per observation for small n: 0 auto, 1/2/4/8 forced (env CFUST_SPLIT)
     double *tau_out;                // density pass (mode 1): responsibilities [n][g] if non-NULL
     int32_t *label_out;             // density pass (mode 1): argmax_i tau_ij [n] if non-NULL
+    int *wperm;                     // [M] lattice points in ascending order of coordinate 0 (chi nodes)
 };
 
 constexpr int TRACE_CAP = 4096;   // device trace ring (power of two); cfust_fit drains it when full

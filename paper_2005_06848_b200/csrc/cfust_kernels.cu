@@ -127,11 +127,44 @@ __device__ __forceinline__ double sov_lane_sum(const double (&binv)[R], const do
 #pragma unroll
     for (int j = 0; j < NPTS; ++j) acc[j] = accw[j] = 0.0;
     const int sub = (SPLIT > 1) ? int(threadIdx.x >> 5) % SPLIT : 0;
-    for (int l0 = lane + sub * 32 * NPTS; l0 < M; l0 += 32 * NPTS * SPLIT) {
-        double s[NPTS], e[NPTS], f[NPTS], z[NPTS][R - 1];
+    // Small-n (SPLIT) mode runs few warps per scheduler, so the L1 latency of each point's chi node
+    // and lattice coordinates stalls the chain that consumes them: load one point block ahead.
+    constexpr bool PF = SPLIT > 1;
+    constexpr int STEP = 32 * NPTS * SPLIT;
+    double sn[NPTS], wn[NPTS][R > 1 ? R - 1 : 1];
+    if constexpr (PF) {
+        const int l1 = lane + sub * 32 * NPTS;
 #pragma unroll
         for (int j = 0; j < NPTS; ++j) {
-            s[j] = __ldg(chi + l0 + 32 * j);
+            sn[j] = __ldg(chi + l1 + 32 * j);
+#pragma unroll
+            for (int k = 1; k < R; ++k) wn[j][k - 1] = __ldg(W + k * M + l1 + 32 * j);
+        }
+    }
+    for (int l0 = lane + sub * 32 * NPTS; l0 < M; l0 += STEP) {
+        double s[NPTS], e[NPTS], f[NPTS], z[NPTS][R - 1], wv[NPTS][R > 1 ? R - 1 : 1];
+        if constexpr (PF) {
+            const int ln = (l0 + STEP < M) ? l0 + STEP : l0;   // (the last block re-reads its own points)
+#pragma unroll
+            for (int j = 0; j < NPTS; ++j) {
+                s[j] = sn[j];
+                sn[j] = __ldg(chi + ln + 32 * j);
+#pragma unroll
+                for (int k = 1; k < R; ++k) {
+                    wv[j][k - 1] = wn[j][k - 1];
+                    wn[j][k - 1] = __ldg(W + k * M + ln + 32 * j);
+                }
+            }
+        } else {
+#pragma unroll
+            for (int j = 0; j < NPTS; ++j) {
+                s[j] = __ldg(chi + l0 + 32 * j);
+#pragma unroll
+                for (int k = 1; k < R; ++k) wv[j][k - 1] = __ldg(W + k * M + l0 + 32 * j);   // lattice coordinate k (table)
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < NPTS; ++j) {
             e[j] = Phi(s[j] * binv[0]);
             f[j] = e[j];
         }
@@ -139,7 +172,7 @@ __device__ __forceinline__ double sov_lane_sum(const double (&binv)[R], const do
         for (int k = 1; k < R; ++k) {
 #pragma unroll
             for (int j = 0; j < NPTS; ++j) {
-                const double w = __ldg(W + k * M + l0 + 32 * j);   // lattice coordinate k (table)
+                const double w = wv[j][k - 1];
                 double u = w * e[j];
                 u = clamp_u(u, UMIN, UMAX);   // clamps (reading A15)
                 z[j][k - 1] = Phiinv(u);
@@ -1859,21 +1892,45 @@ __global__ void __launch_bounds__(32) derive_kernel(DevState s) {
 
 // chi radius nodes: chi[(i*CHI_ROWS + k)*M + l] = sqrt(chi2_{m0+k}^{-1}(w_{l,0}) / (m0+k)), k = 0,1,2;
 // row CHI_LV = log chi2_{m0}^{-1}(w_{l,0}) = log V_l (exact e1, reading R2').
+// Threads take the points in ascending order of w (s.wperm): the lanes of a warp then run the same
+// incomplete-gamma branch (series below a + 1, continued fraction above) for about the same number
+// of terms and Newton steps, instead of both branches and the slowest lane's count.
 __global__ void chi_kernel(DevState s) {
     const int M = s.M;
     const int total = s.g * CHI_ROWS * M;
     for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < total; t += gridDim.x * blockDim.x) {
-        const int l = t % M, ik = t / M, i = ik / CHI_ROWS, k = ik % CHI_ROWS;
+        const int ik = t / M, i = ik / CHI_ROWS, k = ik % CHI_ROWS;
+        const int l = s.wperm ? s.wperm[t % M] : t % M;
         const double w = s.W[l];   // coordinate 0 drives the chi radius
+        double *out = s.chi + size_t(ik) * M + l;
         if (s.family == 1) {   // normal SOV: every radius node is 1
-            s.chi[t] = 1.0;
+            *out = 1.0;
         } else if (k == CHI_LV) {   // only used (and only computed) with exact e1 / the direct estimator
-            if (s.e1_exact || s.direct) s.chi[t] = log(dev_chi2_quantile(w, s.comp[i].m0));
+            if (s.e1_exact || s.direct) *out = log(dev_chi2_quantile(w, s.comp[i].m0));
         } else {
             const double m = s.comp[i].m0 + double(k);
-            s.chi[t] = sqrt(dev_chi2_quantile(w, m) / m);
+            *out = sqrt(dev_chi2_quantile(w, m) / m);
         }
     }
+}
+
+// wperm[rank of W[0][l]] = l (ascending, ties by l): once per context, one thread per point
+__global__ void wperm_kernel(const double *__restrict__ W, int M, int *__restrict__ perm) {
+    __shared__ double tile[256];
+    const int l = blockIdx.x * blockDim.x + threadIdx.x;
+    const double v = (l < M) ? W[l] : 0.0;
+    int rank = 0;
+    for (int j0 = 0; j0 < M; j0 += 256) {
+        __syncthreads();
+        if (j0 + int(threadIdx.x) < M && threadIdx.x < 256) tile[threadIdx.x] = W[j0 + threadIdx.x];
+        __syncthreads();
+        const int jn = min(256, M - j0);
+        for (int j = 0; j < jn; ++j) {
+            const double u = tile[j];
+            rank += (u < v || (u == v && j0 + j < l)) ? 1 : 0;
+        }
+    }
+    if (l < M) perm[rank] = l;
 }
 
 // lattice coordinates W[k][l] = |2 frac((l z_k mod M)/M + shift_k) - 1|, once per context
@@ -2191,7 +2248,7 @@ int launch_derive(const DevState &s, cudaStream_t st) {
 int launch_chi(const DevState &s, cudaStream_t st) {
     if (s.M <= 0) return 0;   // no lattice: q <= 1 without exact e1
     const int total = s.g * CHI_ROWS * s.M;
-    chi_kernel<<<(total + 127) / 128, 128, 0, st>>>(s);
+    chi_kernel<<<(total + 63) / 64, 64, 0, st>>>(s);   // latency bound: spread the warps over the SMs
     return int(cudaGetLastError());
 }
 
@@ -2200,6 +2257,7 @@ int launch_lattice(const DevState &s, cudaStream_t st) {
     const LatticeDev L = make_lattice(s);
     const int total = s.nw * s.M;
     lattice_kernel<<<(total + 127) / 128, 128, 0, st>>>(s, L);
+    if (s.wperm) wperm_kernel<<<(s.M + 255) / 256, 256, 0, st>>>(s.W, s.M, s.wperm);
     return int(cudaGetLastError());
 }
 
