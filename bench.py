@@ -138,9 +138,17 @@ def cpu_baseline(cfg, y, init, budget_s=15.0):
     out = oracle.estep(sub, init, cfg.q, lat, nthreads=cores)
     t = time.perf_counter() - t0
     assert out["rc"] == 0
+    # single-core rate: the same oracle on one thread, a sample sized for ~4 s
+    sub1, _ = _oracle_sample(oracle, cfg, y, init, 1, 4.0)
+    t0 = time.perf_counter()
+    out1 = oracle.estep(sub1, init, cfg.q, lat, nthreads=1)
+    t1 = time.perf_counter() - t0
+    assert out1["rc"] == 0
     return {"value": len(sub) * cfg.g / t, "unit": UNIT, "cores": cores, "kind": "oracle", "cpu": cpu_model(),
             "sample": f"oracle E-step on a strided sample of {len(sub)} of {len(y)} observations x {cfg.g} "
-                      f"components ({t:.1f} s, {cores} OpenMP threads)"}
+                      f"components ({t:.1f} s, {cores} OpenMP threads)",
+            "single_core": {"value": len(sub1) * cfg.g / t1, "unit": UNIT, "cores": 1,
+                            "sample": f"{len(sub1)} observations x {cfg.g} components ({t1:.1f} s, 1 thread)"}}
 
 
 def run_reference(args, cfg):

@@ -1028,6 +1028,9 @@ constexpr int TW = CFUST_TW;   // warps per block of the q = 0 kernel
 #define CFUST_T_P2 2        // phase 2: 1 = w by shuffles + S2 by DADD; 2 = w rows in shared memory + S2 by one DMMA
 #endif
 constexpr int WSTR = 10;   // w row stride (doubles): 80-byte rows, 16-byte aligned, conflict-free 4-row reads
+#ifndef CFUST_T_TAB
+#define CFUST_T_TAB 0       // 1: log1p and exp of the q = 0 E-step from shared-memory tables (measured: no gain, profiles/r02k_cfg3_variants.log)
+#endif
 #ifndef CFUST_T_TMA
 #define CFUST_T_TMA 1       // y tiles staged in shared memory by 1-D bulk copies (double-buffered)
 #endif
@@ -1096,8 +1099,15 @@ __global__ void __launch_bounds__(TW * 32, CFUST_T_MB) estep_t_mma_kernel(EArgs 
     // per warp: 32 rows of this tile's weights w_i = tau_i e2_i (i < G; entries G..7 stay zero)
     double *const wsm = wsm_all + wid * 32 * WSTR;
     for (int t = lane; t < 32 * WSTR; t += 32) wsm[t] = 0.0;
-#else
-    (void)wsm_all;
+#endif
+#if CFUST_T_TAB
+    double2 *const ltab = reinterpret_cast<double2 *>(wsm_all + (CFUST_T_P2 == 2 ? TW * 32 * WSTR : 0));   // [128] (invc_j, log c_j)
+    double *const etab = reinterpret_cast<double *>(ltab + 128);                   // [64] 2^(j/64)
+    for (int t = threadIdx.x; t < 128; t += blockDim.x) {
+        const double invc = (t == 0) ? 1.0 : 1.0 / (1.0 + (t + 0.5) / 128.0);
+        ltab[t] = make_double2(invc, (t == 0) ? 0.0 : -log_unit(invc));
+    }
+    for (int t = threadIdx.x; t < 64; t += blockDim.x) etab[t] = g_EXP2J[t];
 #endif
     __syncthreads();
     for (int t = threadIdx.x; t < G * PMAX; t += blockDim.x)
@@ -1197,15 +1207,27 @@ __global__ void __launch_bounds__(TW * 32, CFUST_T_MB) estep_t_mma_kernel(EArgs 
                 d = fma(t, t, d);
             }
             dd[i] = d;
+#if CFUST_T_TAB
+            l1[i] = nrm ? 0.0 : log1p_tab(d * cp.inv_nu, ltab);
+#else
             l1[i] = nrm ? 0.0 : log1p_pos(d * cp.inv_nu);
+#endif
             lf[i] = cp.logpi + cp.kappa - (nrm ? 0.5 * d : 0.5 * cp.m0 * l1[i]);   // normal: Gaussian component
             mx = fmax(mx, lf[i]);
         }
         double se = 0.0;
 #pragma unroll
+#if CFUST_T_TAB
+        for (int i = 0; i < G; ++i) { lf[i] = exp_tab(lf[i] - mx, etab); se += lf[i]; }   // lf <- exp(lf - max)
+#else
         for (int i = 0; i < G; ++i) { lf[i] = exp_neg(lf[i] - mx); se += lf[i]; }   // lf <- exp(lf - max)
+#endif
         if (valid && mx == -CUDART_INF) atomicOr(A.status, 1);
+#if CFUST_T_TAB
+        if (valid) ll += mx + log_tab(se, ltab);
+#else
         if (valid) ll += mx + log_unit(se);
+#endif
         const double ise = div_fast(1.0, se);
         if (mode == 1) {
             if (A.tau_out && valid) {   // responsibilities and the MAP label (ties -> lowest index)
@@ -2107,7 +2129,8 @@ static int launch_t_mma_g(const DevState &s, EArgs &a, int mode, cudaStream_t st
     const size_t sm = sizeof(CompDev) * G + sizeof(double) * TW * (size_t(G) * s.K + 1)
                       + sizeof(double) * G * (PMAX * PMAX + PMAX)    // L^{-1}, m
                       + 128 + (CFUST_T_TMA ? sizeof(double) * TW * 2 * 32 * PMAX + sizeof(uint64_t) * TW * 2 : 0)   // y tiles, mbarriers
-                      + (CFUST_T_P2 == 2 ? sizeof(double) * TW * 32 * WSTR : 0);   // w rows
+                      + (CFUST_T_P2 == 2 ? sizeof(double) * TW * 32 * WSTR : 0)    // w rows
+                      + (CFUST_T_TAB ? sizeof(double) * (2 * 128 + 64) : 0);          // log / exp tables
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
     if (e != cudaSuccess) return int(e);
     int per_sm = 0;

@@ -117,9 +117,8 @@ __device__ __forceinline__ double horner_eo(const double (&c)[N], double x, doub
 #define CFUST_EXP_TAB 0
 #endif
 
-#if CFUST_EXP_TAB
-// 2^(j/64), j = 0..63, correctly rounded (mpmath, 200 bits); read through L1 (__ldg): a
-// divergent index would serialise a constant-bank load.
+// 2^(j/64), j = 0..63, correctly rounded (mpmath, 200 bits): exp by table (CFUST_EXP_TAB through
+// L1, and the q = 0 kernel from a shared-memory copy).
 __device__ const double g_EXP2J[64] = {
     0x1.0000000000000p+0, 0x1.02c9a3e778061p+0, 0x1.059b0d3158574p+0, 0x1.0874518759bc8p+0,
     0x1.0b5586cf9890fp+0, 0x1.0e3ec32d3d1a2p+0, 0x1.11301d0125b51p+0, 0x1.1429aaea92de0p+0,
@@ -138,7 +137,6 @@ __device__ const double g_EXP2J[64] = {
     0x1.d5818dcfba487p+0, 0x1.da9e603db3285p+0, 0x1.dfc97337b9b5fp+0, 0x1.e502ee78b3ff6p+0,
     0x1.ea4afa2a490dap+0, 0x1.efa1bee615a27p+0, 0x1.f50765b6e4540p+0, 0x1.fa7c1819e90d8p+0,
 };
-#endif
 
 // exp(x) for x <= 709 (x >= -708 exact to ~1 ulp; below: 0, i.e. results < 1e-307 flush).
 // Default: x = k ln2 + r, |r| <= ln2/2: k from the 1.5*2^52 rounding trick, r with a two-part
@@ -220,6 +218,42 @@ __device__ __forceinline__ double log1p_pos(double x) {
     double r;
     asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(z));
     return fma(x - (z - 1.0), r, log_unit(z));
+}
+
+// Table-driven log and exp for the q = 0 E-step (tables in shared memory, filled per block):
+//   log z = e ln2 - log(invc_j) + log1p(r),  r = m invc_j - 1 (one rounding, |r| < 2^-7),
+//     j = the top 7 mantissa bits, invc_j = RN(1 / (1 + (j + 1/2)/128)) (j = 0: exactly 1, so that
+//     log z -> 0 keeps its relative accuracy), log1p(r) to r^8 (relative truncation < 2e-18);
+//   exp x = 2^m 2^(j/64) e^r,  x = (64 m + j) ln2/64 + r, |r| <= ln2/128, e^r - 1 to r^6 (< 3e-20).
+// About 12 FP64 operations each instead of ~20 (log: division + degree-21 series) / 17 (exp).
+__device__ __forceinline__ double log_tab(double z, const double2 *__restrict__ tab) {
+    const int hz = __double2hiint(z);
+    const int e = (hz >> 20) - 1023;
+    const double m = __hiloint2double((hz & 0x000fffff) | 0x3ff00000, __double2loint(z));
+    const double2 t = tab[(hz >> 13) & 127];
+    const double r = fma(m, t.x, -1.0);
+    const double poly = fma(r, fma(r, fma(r, fma(r, fma(r, fma(r, -0.125, 1.0 / 7), -1.0 / 6), 1.0 / 5), -0.25), 1.0 / 3), -0.5);
+    const double ed = double(e);
+    return fma(ed, 0.69314718055994528623, t.y) + fma(ed, 2.3190468138462996e-17, fma(r * r, poly, r));
+}
+// log(1 + x), x >= 0, with the rounding correction of 1 + x (as log1p_pos)
+__device__ __forceinline__ double log1p_tab(double x, const double2 *__restrict__ tab) {
+    const double z = 1.0 + x;
+    double r;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(z));
+    return fma(x - (z - 1.0), r, log_tab(z, tab));
+}
+// exp(x) for x <= 0 (x < -708: 0)
+__device__ __forceinline__ double exp_tab(double x, const double *__restrict__ tab) {
+    const double t = fma(x, 92.33248261689366, 6755399441055744.0);   // 64 / ln2, round to integer k
+    const int k = __double2loint(t);
+    const double kd = t - 6755399441055744.0;
+    const double r = fma(kd, -3.623510646634843e-19, fma(kd, -0.010830424696249145, x));   // x - k ln2/64
+    const double q = r * fma(r, fma(r, fma(r, fma(r, fma(r, 1.0 / 720, 1.0 / 120), 1.0 / 24), 1.0 / 6), 0.5), 1.0);
+    const double T = tab[k & 63];
+    const double p = fma(T, q, T);
+    const double res = __hiloint2double(__double2hiint(p) + (k >> 6) * (1 << 20), __double2loint(p));
+    return (x < -708.0) ? 0.0 : res;
 }
 
 // sqrt(w), w >= 0 finite: rsqrt seed + two Newton steps + one residual correction.

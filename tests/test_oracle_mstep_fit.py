@@ -113,6 +113,33 @@ def test_fit_loglik_monotone_cfg1(orc):
     assert res["trace"][-1] > res["trace"][0]
 
 
+def test_fit_monotone_slack_from_multishift_sd(orc):
+    """C11 with a calibrated slack (monotone EM): along the
+    cfg1 trajectory (n = 1000, 10 iterations) every step satisfies l_{k+1} - l_k >= -4 sqrt(sd_k^2 +
+    sd_{k+1}^2), sd_k the standard deviation of l(Psi^(k)) over 6 independent random lattice shifts
+    (the integration error of the rule); the slack is also checked to be a small fraction of |l|."""
+    cfg, y, init, lat = _setup(orc, 1, 1000)
+    M, z, sh = synth.lattice_inputs(cfg)
+    rng = np.random.default_rng(20261)
+    alts = [orc.Lattice(M, z, (2.0 * rng.integers(0, 1 << 52, size=len(sh)).astype(np.float64) + 1.0) / float(1 << 53))
+            for _ in range(6)]
+    psi, trace, sd = init, [], []
+    for k in range(11):
+        ref = orc.estep(y, psi, cfg.q, lat)
+        trace.append(ref["loglik"])
+        sd.append(np.std([orc.estep(y, psi, cfg.q, a)["loglik"] for a in alts], ddof=1))
+        if k < 10:
+            res = orc.fit(y, psi, cfg.q, lat, max_iter=1)
+            assert res["rc"] == 0
+            psi = res["params"]
+    trace, sd = np.array(trace), np.array(sd)
+    d = np.diff(trace)
+    slack = 4.0 * np.sqrt(sd[:-1] ** 2 + sd[1:] ** 2)
+    assert np.all(sd > 0.0) and np.all(sd < 1e-5 * np.abs(trace)), sd
+    assert np.all(d >= -slack), (d, slack)
+    assert trace[-1] > trace[0]
+
+
 def test_fit_t_mixture_monotone_and_nu_recovery(orc):
     """q=0 (exact EM for the t-mixture): strictly monotone l; nu-hat near 5."""
     cfg = synth.with_(synth.CONFIGS[3], n=10_000, p=2, g=1, nu_lo=5.0, nu_hi=5.0)
