@@ -207,7 +207,8 @@ int cfust_nccl_unique_id(void *out);
  * (the exact code the kernels inline).  which: 0 Phi, 1 Phi^{-1}, 2 exp (x <= 0), 3 log
  * (0 < x <= 1), 4 univariate t CDF with df = aux, 5 chi-square quantile with df = aux,
  * 6 digamma, 7 sqrt, 8 trigamma (the M-step's nu Newton step), 9 log Gamma (x > 0, the M-step's
- * derived constants).  No context needed; CFUST_ECUDA
+ * derived constants), 10 Phi and 11 Phi^{-1} with exp through the 2^(j/64) table (the SOV
+ * loop's optional variant, CFUST_SOV_XT), 12 that table exp (x <= 709).  No context needed; CFUST_ECUDA
  * without a device. */
 int cfust_eval_special(int32_t which, const double *x, double *y, int64_t n, double aux);
 

@@ -20,7 +20,7 @@ from ._native import (CFUST_EDIM, CFUST_EEMPTY, CFUST_EINVAL, CFUST_EMIXPROP, CF
 __all__ = ["CfustEM", "CfustError", "k_stats", "nccl_unique_id", "eval_special", "lib"]
 
 SPECIAL = {"phi": 0, "phiinv": 1, "exp": 2, "log": 3, "t_cdf": 4, "chi2_quantile": 5, "digamma": 6, "sqrt": 7,
-           "trigamma": 8, "lgamma": 9}
+           "trigamma": 8, "lgamma": 9, "phi_xt": 10, "phiinv_xt": 11, "exp_xt": 12}
 
 
 def eval_special(name: str, x, aux: float = 0.0) -> np.ndarray:

@@ -852,7 +852,7 @@ int cfust_get_pairs(cfust_ctx *ctx, const int64_t *idx, int64_t cnt, double *out
 }
 
 int cfust_eval_special(int32_t which, const double *x, double *y, int64_t n, double aux) {
-    if (!x || !y || n < 0 || which < 0 || which > 9) return CFUST_EINVAL;
+    if (!x || !y || n < 0 || which < 0 || which > 12) return CFUST_EINVAL;
     if (n == 0) return CFUST_OK;
     int ndev = 0;
     if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev < 1) return CFUST_ECUDA;

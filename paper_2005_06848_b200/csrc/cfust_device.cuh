@@ -53,6 +53,17 @@ __device__ __forceinline__ double lattice_w(const LatticeDev& L, int l, int k) {
 // Standard normal CDF / quantile used by the SOV loop (cfust_special.cuh).
 __device__ __forceinline__ double Phi(double x) { return Phi_fast(x); }
 __device__ __forceinline__ double Phiinv(double u) { return Phiinv_fast(u); }
+// The SOV loop's copies: XT = exp by the 2^(j/64) table (exp_tab2), chosen per kernel (Tune<Q>::XT).
+template <bool XT>
+__device__ __forceinline__ double Phi_t(double x) { return Phi_x<XT>(x); }
+template <bool XT>
+__device__ __forceinline__ double Phiinv_t(double u) {
+#if CFUST_PHIINV_SEED
+    return Phiinv_seed_x<XT>(u);
+#else
+    return Phiinv_rat(u);
+#endif
+}
 
 // digamma and trigamma for x > 0: upward recurrence to x >= 10, then the Stirling-type asymptotic
 // series through the B_16 (digamma) / B_18 (trigamma) terms (truncation < 1e-17 relative at x = 10).

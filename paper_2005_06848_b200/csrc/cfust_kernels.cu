@@ -103,8 +103,16 @@ struct WarpScratch {
 #ifndef CFUST_MB_Q6
 #define CFUST_MB_Q6 1
 #endif
+// CFUST_SOV_XT = q: the SOV loop of the q kernel takes exp from the 2^(j/64) table (exp_tab2).
+// Off by default: measured at q = 3 (cfg5) -1.3 % E-step time for -12.6 % executed FP64 flops
+// (the loop is latency bound: ncu `wait` ~2.9 per issue either way), q = 2 +1.3 %, q = 4 0
+// (profiles/r02w_ab.log) — not worth a table load in every Phi.
+#ifndef CFUST_SOV_XT
+#define CFUST_SOV_XT 0
+#endif
 template <int Q>
 struct Tune {
+    static constexpr bool XT = Q == CFUST_SOV_XT;
     static constexpr int NP = Q == 1 ? CFUST_NP_Q1 : Q == 2 ? CFUST_NP_Q2 : Q == 3 ? CFUST_NP_Q3
                             : Q == 4 ? CFUST_NP_Q4 : Q == 5 ? CFUST_NP_Q5 : CFUST_NP_Q6;
     static constexpr int MB = Q == 1 ? CFUST_MB_Q1 : Q == 2 ? CFUST_MB_Q2 : Q == 3 ? CFUST_MB_Q3
@@ -114,7 +122,10 @@ struct Tune {
 // WT: also accumulate *wacc += f_l lv_l (exact e1, reading R2': lv = log V node table).
 // SPLIT warps share one observation (small n): warp sub = wid % SPLIT takes the point blocks
 // sub, sub + SPLIT, ... of 32 * NPTS points; split_sum combines the SPLIT warp totals.
-template <int R, int NPTS, bool WT = false, int SPLIT = 1>
+#ifndef CFUST_PF1
+#define CFUST_PF1 0   // 1: one-block-ahead chi / W loads also with one warp per observation (experiment)
+#endif
+template <int R, int NPTS, bool WT = false, int SPLIT = 1, bool XT = false>
 __device__ __forceinline__ double sov_lane_sum(const double (&binv)[R], const double (&Cn)[R * (R - 1) / 2],
                                                const double *__restrict__ chi, const double *__restrict__ W, int M,
                                                int lane, const double *__restrict__ lv = nullptr,
@@ -129,7 +140,7 @@ __device__ __forceinline__ double sov_lane_sum(const double (&binv)[R], const do
     const int sub = (SPLIT > 1) ? int(threadIdx.x >> 5) % SPLIT : 0;
     // Small-n (SPLIT) mode runs few warps per scheduler, so the L1 latency of each point's chi node
     // and lattice coordinates stalls the chain that consumes them: load one point block ahead.
-    constexpr bool PF = SPLIT > 1;
+    constexpr bool PF = SPLIT > 1 || CFUST_PF1;
     constexpr int STEP = 32 * NPTS * SPLIT;
     double sn[NPTS], wn[NPTS][R > 1 ? R - 1 : 1];
     if constexpr (PF) {
@@ -165,7 +176,7 @@ __device__ __forceinline__ double sov_lane_sum(const double (&binv)[R], const do
         }
 #pragma unroll
         for (int j = 0; j < NPTS; ++j) {
-            e[j] = Phi(s[j] * binv[0]);
+            e[j] = Phi_t<XT>(s[j] * binv[0]);
             f[j] = e[j];
         }
 #pragma unroll
@@ -175,11 +186,11 @@ __device__ __forceinline__ double sov_lane_sum(const double (&binv)[R], const do
                 const double w = wv[j][k - 1];
                 double u = w * e[j];
                 u = clamp_u(u, UMIN, UMAX);   // clamps (reading A15)
-                z[j][k - 1] = Phiinv(u);
+                z[j][k - 1] = Phiinv_t<XT>(u);
                 double a = s[j] * binv[k];
 #pragma unroll
                 for (int t = 0; t < k; ++t) a -= Cn[(k * (k - 1)) / 2 + t] * z[j][t];
-                e[j] = Phi(a);
+                e[j] = Phi_t<XT>(a);
                 f[j] *= e[j];
             }
         }
@@ -256,7 +267,7 @@ __device__ __forceinline__ double split_sum(double v) {
 
 // T_R(b; 0, S, m): R = 0 -> 1; R = 1 -> univariate t CDF; R >= 2 -> lattice rule with
 // univariate-prioritisation reordering (ascending b_k / sqrt(S_kk), stable; reading A13).
-template <int R, int NP, int SPLIT = 1>
+template <int R, int NP, int SPLIT = 1, bool XT = false>
 __device__ __noinline__ double T_eval(const double *b, const double *S, int lds, double m, double lbt,
                                       const double *__restrict__ chi, const double *__restrict__ W, int M,
                                       int lane) {
@@ -267,14 +278,30 @@ __device__ __noinline__ double T_eval(const double *b, const double *S, int lds,
     } else {
         double binv[R], Cn[R * (R - 1) / 2];
         if (!sov_setup<R>(b, S, lds, binv, Cn)) return CUDART_NAN;
-        const double acc = sov_lane_sum<R, NP, false, SPLIT>(binv, Cn, chi, W, M, lane);
+        const double acc = sov_lane_sum<R, NP, false, SPLIT, XT>(binv, Cn, chi, W, M, lane);
         return split_sum<SPLIT>(warp_sum(acc)) / double(M);
     }
 }
 
+// NT >= 2 univariate T_1 values (T_eval<1> of argument arg = b / sqrt(S)) for one pair, one per
+// lane (lane i < NT evaluates arg[i], the others repeat arg[0]) and broadcast: the warp-uniform
+// continued fractions run side by side instead of one after another (q = 2: T_{q-1}, q = 3:
+// T_{q-2}).  Bitwise the values T_eval<1> returns.
+#ifndef CFUST_T1_LANES
+#define CFUST_T1_LANES 1
+#endif
+template <int NT>
+__device__ __forceinline__ void T1_lanes(const double *arg, double m, double lbt, int lane, double *out) {
+    const int i = (lane < NT) ? lane : 0;
+    const double x = arg[i];
+    const double v = isinf(m) ? Phi(x) : dev_t_cdf(x, m, lbt);
+#pragma unroll
+    for (int k = 0; k < NT; ++k) out[k] = __shfl_sync(0xffffffffu, v, k);
+}
+
 // T_R on the lattice together with *wsum = (1/M) sum_l f_l lv_l over the same points (exact e1,
 // reading R2'); R = 1 is evaluated on the lattice here too (f_l = Phi(s_l b / sqrt(S))).
-template <int R, int NP, int SPLIT = 1>
+template <int R, int NP, int SPLIT = 1, bool XT = false>
 __device__ __noinline__ double T_eval_w(const double *b, const double *S, int lds, const double *__restrict__ chi,
                                         const double *__restrict__ lv, const double *__restrict__ W, int M, int lane,
                                         double *wsum) {
@@ -284,14 +311,14 @@ __device__ __noinline__ double T_eval_w(const double *b, const double *S, int ld
         const double bs = b[0] / sqrt(S[0]);
         const int sub = (SPLIT > 1) ? int(threadIdx.x >> 5) % SPLIT : 0;
         for (int l = lane + 32 * sub; l < M; l += 32 * SPLIT) {
-            const double f = Phi(__ldg(chi + l) * bs);
+            const double f = Phi_t<XT>(__ldg(chi + l) * bs);
             acc += f;
             accw = fma(f, __ldg(lv + l), accw);
         }
     } else {
         double binv[R], Cn[R * (R - 1) / 2];
         if (!sov_setup<R>(b, S, lds, binv, Cn)) { *wsum = CUDART_NAN; return CUDART_NAN; }
-        acc = sov_lane_sum<R, NP, true, SPLIT>(binv, Cn, chi, W, M, lane, lv, &accw);
+        acc = sov_lane_sum<R, NP, true, SPLIT, XT>(binv, Cn, chi, W, M, lane, lv, &accw);
     }
     *wsum = split_sum<SPLIT>(warp_sum(accw)) / double(M);
     return split_sum<SPLIT>(warp_sum(acc)) / double(M);
@@ -492,11 +519,11 @@ __device__ void pair_eval(const CompDev &cp, int p, const double *__restrict__ W
     double T0, e1x = 0.0;
     if (MODE != 1 && e1_exact) {   // exact e1 = (sum f lv)/(sum f) - log rho on T0's points (R2')
         double wsum;
-        const double T0lat = T_eval_w<Q, Tune<Q>::NP, SPLIT>(ws.b, cp.Lam, QMAX, chi, chi + CHI_LV * M, W, M, lane, &wsum);
+        const double T0lat = T_eval_w<Q, Tune<Q>::NP, SPLIT, Tune<Q>::XT>(ws.b, cp.Lam, QMAX, chi, chi + CHI_LV * M, W, M, lane, &wsum);
         T0 = (Q == 1) ? T_eval<1, 1>(ws.b, cp.Lam, QMAX, m0, cp.lbt[0], chi, W, M, lane) : T0lat;   // density: exact T_1
         e1x = wsum / T0lat - log(rho);
     } else {
-        T0 = T_eval<Q, Tune<Q>::NP, SPLIT>(ws.b, cp.Lam, QMAX, mT0, cp.lbt[0], chi, W, M, lane);
+        T0 = T_eval<Q, Tune<Q>::NP, SPLIT, Tune<Q>::XT>(ws.b, cp.Lam, QMAX, mT0, cp.lbt[0], chi, W, M, lane);
     }
     if (MODE == 1) {
         res[0] = (T0 >= TMIN) ? Q * CUDART_LN2 + logt + log(T0) : -CUDART_INF;
@@ -507,7 +534,7 @@ __device__ void pair_eval(const CompDev &cp, int p, const double *__restrict__ W
         const double sq2 = sqrt((m0 + 2.0) / rho);
 #pragma unroll
         for (int k = 0; k < Q; ++k) ws.b[k] = c[k] * sq2;
-        T2 = T_eval<Q, Tune<Q>::NP, SPLIT>(ws.b, cp.Lam, QMAX, m0 + 2.0, cp.lbt[2], chi + CHI_M2 * M, W, M, lane);
+        T2 = T_eval<Q, Tune<Q>::NP, SPLIT, Tune<Q>::XT>(ws.b, cp.Lam, QMAX, m0 + 2.0, cp.lbt[2], chi + CHI_M2 * M, W, M, lane);
     }
     res[1] = nrm ? 0.0 : cp.psi_half_m0 - log(0.5 * rho) - m0 / rho;      // e1 - e2, reading A5
     if (!(T0 >= TMIN)) {                                        // reading A16
@@ -568,20 +595,46 @@ __device__ void pair_eval(const CompDev &cp, int p, const double *__restrict__ W
                     }
                     ++ib;
                 }
-                const double val = T_eval<Q2, Tune<Q>::NP, SPLIT>(ws.bc, ws.Sc, QMAX, mT0, cp.lbt[0], chi, W, M, lane);
-                ws.Tkt[k * QMAX + t] = val;
-                ws.Tkt[t * QMAX + k] = val;            // symmetric in {k, t} (A17)
+                if constexpr (Q2 == 1 && CFUST_T1_LANES) {
+                    ws.Tkt[t * QMAX + k] = ws.bc[0] / sqrt(ws.Sc[0]);   // T_1 argument, evaluated below
+                } else {
+                    const double val = T_eval<Q2, Tune<Q>::NP, SPLIT, Tune<Q>::XT>(ws.bc, ws.Sc, QMAX, mT0, cp.lbt[0], chi, W, M, lane);
+                    ws.Tkt[k * QMAX + t] = val;
+                    ws.Tkt[t * QMAX + k] = val;            // symmetric in {k, t} (A17)
+                }
             }
+        if constexpr (Q2 == 1 && CFUST_T1_LANES) {   // q = 3: the three T_1 side by side; arguments at (t, k), t > k
+            __syncwarp();
+            const double arg[3] = {ws.Tkt[1 * QMAX + 0], ws.Tkt[2 * QMAX + 0], ws.Tkt[2 * QMAX + 1]};
+            double val[3];
+            T1_lanes<3>(arg, mT0, cp.lbt[0], lane, val);
+            __syncwarp();
+            ws.Tkt[0 * QMAX + 1] = ws.Tkt[1 * QMAX + 0] = val[0];
+            ws.Tkt[0 * QMAX + 2] = ws.Tkt[2 * QMAX + 0] = val[1];
+            ws.Tkt[1 * QMAX + 2] = ws.Tkt[2 * QMAX + 1] = val[2];
+            __syncwarp();
+        }
     }
     // T_{q-1}(c~(k); 0, S~(k), m0+1) and h_k = phi_k T~(k)
     double h[Q];
+    if constexpr (Q1 == 1 && CFUST_T1_LANES) {   // q = 2: both T_1 side by side
+        const double arg[2] = {ws.ct[0][0] / sqrt(ws.St[0][0]), ws.ct[1][0] / sqrt(ws.St[1][0])};
+        double tk[2];
+        T1_lanes<2>(arg, nrm ? CUDART_INF : m0 + 1.0, cp.lbt[1], lane, tk);
 #pragma unroll
-    for (int k = 0; k < Q; ++k) {
-        double tk = 1.0;
-        if constexpr (Q >= 2)
-            tk = T_eval<Q1, Tune<Q>::NP, SPLIT>(ws.ct[k], ws.St[k], QMAX, nrm ? CUDART_INF : m0 + 1.0, cp.lbt[1], chi + CHI_M1 * M, W, M, lane);
-        ws.Tk[k] = tk;
-        h[k] = ws.phi[k] * tk;
+        for (int k = 0; k < Q; ++k) {
+            ws.Tk[k] = tk[k];
+            h[k] = ws.phi[k] * tk[k];
+        }
+    } else {
+#pragma unroll
+        for (int k = 0; k < Q; ++k) {
+            double tk = 1.0;
+            if constexpr (Q >= 2)
+                tk = T_eval<Q1, Tune<Q>::NP, SPLIT, Tune<Q>::XT>(ws.ct[k], ws.St[k], QMAX, nrm ? CUDART_INF : m0 + 1.0, cp.lbt[1], chi + CHI_M1 * M, W, M, lane);
+            ws.Tk[k] = tk;
+            h[k] = ws.phi[k] * tk;
+        }
     }
     // E1 = c T2 + S' h
     double E1[Q];
@@ -1983,6 +2036,9 @@ __global__ void special_kernel(int which, const double *__restrict__ x, double *
             case 7: r = sqrt_fast(v); break;
             case 8: r = dev_trigamma(v); break;
             case 9: r = dev_lgamma_pos(v); break;
+            case 10: r = Phi_t<true>(v); break;
+            case 11: r = Phiinv_t<true>(v); break;
+            case 12: r = exp_tab2(v, 0.0); break;
             default: r = CUDART_NAN;
         }
         y[t] = r;

@@ -271,14 +271,38 @@ __device__ __forceinline__ double sqrt_fast(double w) {
 #endif
 }
 
+// exp(xh + xl) (as exp_neg2) with 2^(j/64) from the 64-entry table through L1:
+// x = (64 m + j) ln2/64 + r, |r| <= ln2/128, e^r - 1 to r^5/120 (truncation < 4e-17): 9 FP64
+// operations and one table load (off the dependent chain: the load runs beside the polynomial)
+// instead of the 16 of the degree-11 polynomial.  The SOV loop of the kernel CFUST_SOV_XT = q uses
+// it (Tune<q>::XT; off by default: -1.3 % at q = 3, +1.3 % at q = 2, profiles/r02w_ab.log).
+__device__ __forceinline__ double exp_tab2(double xh, double xl) {
+    const double t = fma(xh, 92.33248261689366, 6755399441055744.0);   // 64 / ln2, round to integer k
+    const int k = __double2loint(t);
+    const double kd = t - 6755399441055744.0;
+    const double r = fma(kd, -3.623510646634843e-19, fma(kd, -0.010830424696249145, xh)) + xl;
+    const double T = __ldg(&g_EXP2J[k & 63]);
+    const double q = r * fma(r, fma(r, fma(r, fma(r, 1.0 / 120.0, 1.0 / 24.0), 1.0 / 6.0), 0.5), 1.0);
+    const double p = fma(T, q, T);
+    const double res = __hiloint2double(__double2hiint(p) + (k >> 6) * (1 << 20), __double2loint(p));
+    return (xh < -708.0) ? 0.0 : res;
+}
+template <bool XT>
+__device__ __forceinline__ double exp_sov(double xh, double xl) {
+    if constexpr (XT) return exp_tab2(xh, xl);
+    else return exp_neg2(xh, xl);
+}
+
 // Phi(x) = P(X <= x), X ~ N(0,1); relative accuracy in the lower tail (to ~1e-307), absolute
 // accuracy for x > 0.  x^2 is split exactly (hi + lo) so the exponent carries no rounding.
-__device__ __forceinline__ double Phi_fast(double x) {
+// XT: exp by table (exp_tab2).
+template <bool XT>
+__device__ __forceinline__ double Phi_x(double x) {
     const double fx = fabs(x);
     const double ax = (fx < 40.0) ? fx : 40.0;   // exp(-800) = 0: Phi is exactly 0 or 1 beyond
     const double hi = ax * ax;
     const double lo = fma(ax, ax, -hi);
-    const double e = exp_neg2(-0.5 * hi, -0.5 * lo);
+    const double e = exp_sov<XT>(-0.5 * hi, -0.5 * lo);
 #if CFUST_HORNER
     const double t = e * div_rat(horner_eo(c_PH_P, ax, hi), horner_eo(c_PH_Q, ax, hi));
 #else
@@ -291,6 +315,7 @@ __device__ __forceinline__ double Phi_fast(double x) {
     return (x < 0.0) ? t : 1.0 - t;
 #endif
 }
+__device__ __forceinline__ double Phi_fast(double x) { return Phi_x<false>(x); }
 
 // Phi^{-1}(u), 0 < u < 1.  1 - u is exact for u >= 1/2; 2t is exact; log(2t) is accurate to
 // ~1 ulp of its value, so w keeps full relative precision as u -> 1/2.
@@ -361,7 +386,8 @@ __device__ __forceinline__ float seed_U32(float v) {
 //   No log, no sqrt, one division in FP64 (vs log + sqrt + a (14,15) rational + division).
 //   Accuracy (CPU emulation, tests/test_special_coeffs.py): relative 3e-16 for |x| >= 1,
 //   absolute 4e-16 below (the SOV loop consumes z only through a = s b - sum C z).
-__device__ __forceinline__ double Phiinv_seed(double u) {
+template <bool XT>
+__device__ __forceinline__ double Phiinv_seed_x(double u) {
     const double uc = 1.0 - u;
     const double t = (u < uc) ? u : uc;
     const int hx = __double2hiint(t);
@@ -373,7 +399,7 @@ __device__ __forceinline__ double Phiinv_seed(double u) {
     const double ax = fmin(double(w * seed_U32(v)), 37.5);                   // |z0|
     const double hi = ax * ax;
     const double lo = fma(ax, ax, -hi);
-    const double ep = exp_neg2(0.5 * hi, 0.5 * lo);                         // e^{z0^2/2} (valid to +709)
+    const double ep = exp_sov<XT>(0.5 * hi, 0.5 * lo);                      // e^{z0^2/2} (valid to +709)
     const double R = div_rat(horner_eo(c_PH_P, ax, hi), horner_eo(c_PH_Q, ax, hi));
     const double r = 2.5066282746310002 * fma(t, ep, -R);
     const double x = fma(r, fma(r, fma(r, fma(hi, 1.0 / 3.0, 1.0 / 6.0), -0.5 * ax), 1.0), -ax);
@@ -383,6 +409,7 @@ __device__ __forceinline__ double Phiinv_seed(double u) {
     return (u < 0.5) ? x : -x;
 #endif
 }
+__device__ __forceinline__ double Phiinv_seed(double u) { return Phiinv_seed_x<false>(u); }
 
 // u clamped to [UMIN, UMAX] for u >= 0 (u = w e with w, e in [0, 1]); with CFUST_INTSEL on the
 // integer image (non-negative doubles order like their bit patterns).

@@ -22,9 +22,10 @@ def cf():
     return m
 
 
-def test_phi(cf):
+@pytest.mark.parametrize("name", ["phi", "phi_xt"])
+def test_phi(cf, name):
     x = np.concatenate([np.linspace(-37.5, 8.5, 20001), [0.0, -1e-300, 1e-300, -45.0, 45.0, -1e30, 1e30]])
-    y = cf.eval_special("phi", x)
+    y = cf.eval_special(name, x)
     ref = np.array([float(mp.ncdf(v)) for v in x])
     ok = np.abs(x) <= 37.5
     rel = np.abs(y[ok] - ref[ok]) / ref[ok] / (1.0 + 0.5 * x[ok] ** 2)
@@ -32,10 +33,11 @@ def test_phi(cf):
     assert y[-4] == 0.0 and y[-3] == 1.0 and y[-2] == 0.0 and y[-1] == 1.0
 
 
-def test_phiinv(cf):
+@pytest.mark.parametrize("name", ["phiinv", "phiinv_xt"])
+def test_phiinv(cf, name):
     u = np.concatenate([np.logspace(-300, -1, 3000), np.linspace(0.001, 0.999, 3001), 1 - np.logspace(-16, -1, 500),
                         [0.5, np.nextafter(0.5, 0), np.nextafter(0.5, 1)]])
-    z = cf.eval_special("phiinv", u)
+    z = cf.eval_special(name, u)
     for ui, zi in zip(u[::7], z[::7]):
         ref = mp.mpf(float(sp.ndtri(ui)))
         for _ in range(6):
@@ -45,6 +47,16 @@ def test_phiinv(cf):
         err = abs(zi - ref) / max(abs(ref), mp.mpf(1))
         assert err < 3e-15, (ui, zi, ref)
     assert z[-3] == 0.0
+
+
+def test_exp_table(cf):
+    # the SOV loop's optional table exp (CFUST_SOV_XT builds): negative arguments (Phi) and positive ones up to
+    # 703 (e^{z0^2/2} of the quantile correction, |z0| <= 37.5)
+    x = np.concatenate([-np.logspace(-12, np.log10(708), 5000), np.logspace(-12, np.log10(703.2), 5000), [0.0]])
+    y = cf.eval_special("exp_xt", x)
+    ref = np.array([float(mp.exp(mp.mpf(float(v)))) for v in x])
+    assert np.max(np.abs(y - ref) / ref) < 5e-16
+    assert cf.eval_special("exp_xt", np.array([-709.0, -745.0]))[1] == 0.0
 
 
 def test_exp_log_sqrt(cf):
