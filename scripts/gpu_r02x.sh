@@ -18,3 +18,5 @@ rm -f gpurun_out/r02x_cfg5_slice.ncu-rep
 timeout 600 python scripts/iter_time.py > gpurun_out/r02x_iter_time.log 2>&1; echo "exit $?" >> gpurun_out/r02x_iter_time.log
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/r02x_smoke.log 2>&1; echo "smoke exit $?" >> gpurun_out/r02x_smoke.log
 timeout 1500 python -m pytest tests -m gpu -q --durations=10 > gpurun_out/r02x_pytest_gpu.log 2>&1; echo "pytest exit $?" >> gpurun_out/r02x_pytest_gpu.log
+timeout 900 python bench.py > gpurun_out/r02x_bench.log 2> gpurun_out/r02x_bench.err; echo "bench exit $?" >> gpurun_out/r02x_bench.err
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/r02x_launches_bench_cfg5.csv python bench.py --steps 3 --warmup 3 --no-cpu-baseline > gpurun_out/r02x_ncu_bench.log 2>&1; echo "ncu exit $?" >> gpurun_out/r02x_ncu_bench.log
