@@ -110,9 +110,17 @@ struct WarpScratch {
 #ifndef CFUST_SOV_XT
 #define CFUST_SOV_XT 0
 #endif
+// CFUST_PF1_MASK bit q: the q kernel loads each point block's chi node / lattice coordinates one
+// block ahead also with one warp per observation (SPLIT = 1; the SPLIT > 1 modes always do).  Same
+// values in the same order: results are bitwise unchanged.  Measured (profiles/r02x_ab.log): q = 3
+// (cfg5) -2.5 % E-step time, q = 2 +2.3 %; q = 4 / 6: profiles/r02z_ab.log.
+#ifndef CFUST_PF1_MASK
+#define CFUST_PF1_MASK (1 << 3)
+#endif
 template <int Q>
 struct Tune {
     static constexpr bool XT = Q == CFUST_SOV_XT;
+    static constexpr bool PF = (CFUST_PF1_MASK >> Q) & 1;
     static constexpr int NP = Q == 1 ? CFUST_NP_Q1 : Q == 2 ? CFUST_NP_Q2 : Q == 3 ? CFUST_NP_Q3
                             : Q == 4 ? CFUST_NP_Q4 : Q == 5 ? CFUST_NP_Q5 : CFUST_NP_Q6;
     static constexpr int MB = Q == 1 ? CFUST_MB_Q1 : Q == 2 ? CFUST_MB_Q2 : Q == 3 ? CFUST_MB_Q3
@@ -122,10 +130,7 @@ struct Tune {
 // WT: also accumulate *wacc += f_l lv_l (exact e1, reading R2': lv = log V node table).
 // SPLIT warps share one observation (small n): warp sub = wid % SPLIT takes the point blocks
 // sub, sub + SPLIT, ... of 32 * NPTS points; split_sum combines the SPLIT warp totals.
-#ifndef CFUST_PF1
-#define CFUST_PF1 0   // 1: one-block-ahead chi / W loads also with one warp per observation (experiment)
-#endif
-template <int R, int NPTS, bool WT = false, int SPLIT = 1, bool XT = false>
+template <int R, int NPTS, bool WT = false, int SPLIT = 1, bool XT = false, bool PF1 = false>
 __device__ __forceinline__ double sov_lane_sum(const double (&binv)[R], const double (&Cn)[R * (R - 1) / 2],
                                                const double *__restrict__ chi, const double *__restrict__ W, int M,
                                                int lane, const double *__restrict__ lv = nullptr,
@@ -140,7 +145,7 @@ __device__ __forceinline__ double sov_lane_sum(const double (&binv)[R], const do
     const int sub = (SPLIT > 1) ? int(threadIdx.x >> 5) % SPLIT : 0;
     // Small-n (SPLIT) mode runs few warps per scheduler, so the L1 latency of each point's chi node
     // and lattice coordinates stalls the chain that consumes them: load one point block ahead.
-    constexpr bool PF = SPLIT > 1 || CFUST_PF1;
+    constexpr bool PF = SPLIT > 1 || PF1;
     constexpr int STEP = 32 * NPTS * SPLIT;
     double sn[NPTS], wn[NPTS][R > 1 ? R - 1 : 1];
     if constexpr (PF) {
@@ -267,7 +272,7 @@ __device__ __forceinline__ double split_sum(double v) {
 
 // T_R(b; 0, S, m): R = 0 -> 1; R = 1 -> univariate t CDF; R >= 2 -> lattice rule with
 // univariate-prioritisation reordering (ascending b_k / sqrt(S_kk), stable; reading A13).
-template <int R, int NP, int SPLIT = 1, bool XT = false>
+template <int R, int NP, int SPLIT = 1, bool XT = false, bool PF1 = false>
 __device__ __noinline__ double T_eval(const double *b, const double *S, int lds, double m, double lbt,
                                       const double *__restrict__ chi, const double *__restrict__ W, int M,
                                       int lane) {
@@ -278,7 +283,7 @@ __device__ __noinline__ double T_eval(const double *b, const double *S, int lds,
     } else {
         double binv[R], Cn[R * (R - 1) / 2];
         if (!sov_setup<R>(b, S, lds, binv, Cn)) return CUDART_NAN;
-        const double acc = sov_lane_sum<R, NP, false, SPLIT, XT>(binv, Cn, chi, W, M, lane);
+        const double acc = sov_lane_sum<R, NP, false, SPLIT, XT, PF1>(binv, Cn, chi, W, M, lane);
         return split_sum<SPLIT>(warp_sum(acc)) / double(M);
     }
 }
@@ -301,7 +306,7 @@ __device__ __forceinline__ void T1_lanes(const double *arg, double m, double lbt
 
 // T_R on the lattice together with *wsum = (1/M) sum_l f_l lv_l over the same points (exact e1,
 // reading R2'); R = 1 is evaluated on the lattice here too (f_l = Phi(s_l b / sqrt(S))).
-template <int R, int NP, int SPLIT = 1, bool XT = false>
+template <int R, int NP, int SPLIT = 1, bool XT = false, bool PF1 = false>
 __device__ __noinline__ double T_eval_w(const double *b, const double *S, int lds, const double *__restrict__ chi,
                                         const double *__restrict__ lv, const double *__restrict__ W, int M, int lane,
                                         double *wsum) {
@@ -318,7 +323,7 @@ __device__ __noinline__ double T_eval_w(const double *b, const double *S, int ld
     } else {
         double binv[R], Cn[R * (R - 1) / 2];
         if (!sov_setup<R>(b, S, lds, binv, Cn)) { *wsum = CUDART_NAN; return CUDART_NAN; }
-        acc = sov_lane_sum<R, NP, true, SPLIT, XT>(binv, Cn, chi, W, M, lane, lv, &accw);
+        acc = sov_lane_sum<R, NP, true, SPLIT, XT, PF1>(binv, Cn, chi, W, M, lane, lv, &accw);
     }
     *wsum = split_sum<SPLIT>(warp_sum(accw)) / double(M);
     return split_sum<SPLIT>(warp_sum(acc)) / double(M);
@@ -519,11 +524,11 @@ __device__ void pair_eval(const CompDev &cp, int p, const double *__restrict__ W
     double T0, e1x = 0.0;
     if (MODE != 1 && e1_exact) {   // exact e1 = (sum f lv)/(sum f) - log rho on T0's points (R2')
         double wsum;
-        const double T0lat = T_eval_w<Q, Tune<Q>::NP, SPLIT, Tune<Q>::XT>(ws.b, cp.Lam, QMAX, chi, chi + CHI_LV * M, W, M, lane, &wsum);
+        const double T0lat = T_eval_w<Q, Tune<Q>::NP, SPLIT, Tune<Q>::XT, Tune<Q>::PF>(ws.b, cp.Lam, QMAX, chi, chi + CHI_LV * M, W, M, lane, &wsum);
         T0 = (Q == 1) ? T_eval<1, 1>(ws.b, cp.Lam, QMAX, m0, cp.lbt[0], chi, W, M, lane) : T0lat;   // density: exact T_1
         e1x = wsum / T0lat - log(rho);
     } else {
-        T0 = T_eval<Q, Tune<Q>::NP, SPLIT, Tune<Q>::XT>(ws.b, cp.Lam, QMAX, mT0, cp.lbt[0], chi, W, M, lane);
+        T0 = T_eval<Q, Tune<Q>::NP, SPLIT, Tune<Q>::XT, Tune<Q>::PF>(ws.b, cp.Lam, QMAX, mT0, cp.lbt[0], chi, W, M, lane);
     }
     if (MODE == 1) {
         res[0] = (T0 >= TMIN) ? Q * CUDART_LN2 + logt + log(T0) : -CUDART_INF;
@@ -534,7 +539,7 @@ __device__ void pair_eval(const CompDev &cp, int p, const double *__restrict__ W
         const double sq2 = sqrt((m0 + 2.0) / rho);
 #pragma unroll
         for (int k = 0; k < Q; ++k) ws.b[k] = c[k] * sq2;
-        T2 = T_eval<Q, Tune<Q>::NP, SPLIT, Tune<Q>::XT>(ws.b, cp.Lam, QMAX, m0 + 2.0, cp.lbt[2], chi + CHI_M2 * M, W, M, lane);
+        T2 = T_eval<Q, Tune<Q>::NP, SPLIT, Tune<Q>::XT, Tune<Q>::PF>(ws.b, cp.Lam, QMAX, m0 + 2.0, cp.lbt[2], chi + CHI_M2 * M, W, M, lane);
     }
     res[1] = nrm ? 0.0 : cp.psi_half_m0 - log(0.5 * rho) - m0 / rho;      // e1 - e2, reading A5
     if (!(T0 >= TMIN)) {                                        // reading A16
@@ -598,7 +603,7 @@ __device__ void pair_eval(const CompDev &cp, int p, const double *__restrict__ W
                 if constexpr (Q2 == 1 && CFUST_T1_LANES) {
                     ws.Tkt[t * QMAX + k] = ws.bc[0] / sqrt(ws.Sc[0]);   // T_1 argument, evaluated below
                 } else {
-                    const double val = T_eval<Q2, Tune<Q>::NP, SPLIT, Tune<Q>::XT>(ws.bc, ws.Sc, QMAX, mT0, cp.lbt[0], chi, W, M, lane);
+                    const double val = T_eval<Q2, Tune<Q>::NP, SPLIT, Tune<Q>::XT, Tune<Q>::PF>(ws.bc, ws.Sc, QMAX, mT0, cp.lbt[0], chi, W, M, lane);
                     ws.Tkt[k * QMAX + t] = val;
                     ws.Tkt[t * QMAX + k] = val;            // symmetric in {k, t} (A17)
                 }
@@ -631,7 +636,7 @@ __device__ void pair_eval(const CompDev &cp, int p, const double *__restrict__ W
         for (int k = 0; k < Q; ++k) {
             double tk = 1.0;
             if constexpr (Q >= 2)
-                tk = T_eval<Q1, Tune<Q>::NP, SPLIT, Tune<Q>::XT>(ws.ct[k], ws.St[k], QMAX, nrm ? CUDART_INF : m0 + 1.0, cp.lbt[1], chi + CHI_M1 * M, W, M, lane);
+                tk = T_eval<Q1, Tune<Q>::NP, SPLIT, Tune<Q>::XT, Tune<Q>::PF>(ws.ct[k], ws.St[k], QMAX, nrm ? CUDART_INF : m0 + 1.0, cp.lbt[1], chi + CHI_M1 * M, W, M, lane);
             ws.Tk[k] = tk;
             h[k] = ws.phi[k] * tk;
         }
