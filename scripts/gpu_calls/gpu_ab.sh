@@ -1,4 +1,4 @@
-# usage: bash scripts/gpu_ab.sh libA libB ...  (paper_2005_06848_b200/libcfust_<name>.so or "cur" = libcfust.so)
+# usage: bash scripts/gpu_calls/gpu_ab.sh libA libB ...  (paper_2005_06848_b200/libcfust_<name>.so or "cur" = libcfust.so)
 # E-step ms of each build on cfg1 / cfg5 / cfg2 / cfg4 slices, interleaved, 2 rounds -> gpurun_out/ab.log
 cd $GRAFT_REPO_ROOT; mkdir -p gpurun_out
 for r in 1 2; do

@@ -1,4 +1,4 @@
-# usage: bash scripts/gpu_cfg3.sh name1 name2 ...  (paper_2005_06848_b200/libcfust_<name>.so)
+# usage: bash scripts/gpu_calls/gpu_cfg3.sh name1 name2 ...  (paper_2005_06848_b200/libcfust_<name>.so)
 # q = 0 parity for each build, then the cfg3 E-step time (3 repetitions) -> gpurun_out/cfg3.log
 cd $GRAFT_REPO_ROOT; mkdir -p gpurun_out
 for v in "$@"; do

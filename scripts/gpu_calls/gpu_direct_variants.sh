@@ -1,4 +1,4 @@
-# E-step timing of the SOV-direct estimator for experiment builds: bash scripts/gpu_direct_variants.sh lib...
+# E-step timing of the SOV-direct estimator for experiment builds: bash scripts/gpu_calls/gpu_direct_variants.sh lib...
 cd $GRAFT_REPO_ROOT; mkdir -p gpurun_out
 for v in "$@"; do
   echo "== $v" >> gpurun_out/dvariants.log

@@ -1,4 +1,4 @@
-# usage: bash scripts/gpu_round.sh [tests|bench|prof|all] ; outputs under gpurun_out/
+# usage: bash scripts/gpu_calls/gpu_round.sh [tests|bench|prof|all] ; outputs under gpurun_out/
 cd $GRAFT_REPO_ROOT
 mkdir -p gpurun_out
 what=${1:-all}

@@ -1,4 +1,4 @@
-# q = 0 kernel timing for experiment builds: bash scripts/gpu_t_variants.sh lib...
+# q = 0 kernel timing for experiment builds: bash scripts/gpu_calls/gpu_t_variants.sh lib...
 cd $GRAFT_REPO_ROOT; mkdir -p gpurun_out
 for v in "$@"; do
   echo "== $v" >> gpurun_out/tvariants.log

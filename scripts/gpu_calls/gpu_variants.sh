@@ -1,4 +1,4 @@
-# usage: bash scripts/gpu_variants.sh lib1 lib2 ...   (names of paper_2005_06848_b200/libcfust_<name>.so)
+# usage: bash scripts/gpu_calls/gpu_variants.sh lib1 lib2 ...   (names of paper_2005_06848_b200/libcfust_<name>.so)
 # E-step timing of experiment builds on cfg2 / cfg5 / cfg4 slices -> gpurun_out/variants.log
 cd $GRAFT_REPO_ROOT; mkdir -p gpurun_out
 for v in "$@"; do
