@@ -113,9 +113,9 @@ struct WarpScratch {
 // CFUST_PF1_MASK bit q: the q kernel loads each point block's chi node / lattice coordinates one
 // block ahead also with one warp per observation (SPLIT = 1; the SPLIT > 1 modes always do).  Same
 // values in the same order: results are bitwise unchanged.  Measured (profiles/r02x_ab.log): q = 3
-// (cfg5) -2.5 % E-step time, q = 2 +2.3 %; q = 4 / 6: profiles/r02z_ab.log.
+// (cfg5) -2.6 % E-step time, q = 4 (cfg2) -1.6 %, q = 2 +2.7 %, q = 6 +25 % (spills): profiles/r02z_ab.log.
 #ifndef CFUST_PF1_MASK
-#define CFUST_PF1_MASK (1 << 3)
+#define CFUST_PF1_MASK ((1 << 3) | (1 << 4))
 #endif
 template <int Q>
 struct Tune {
