@@ -60,7 +60,8 @@ def parse_rep(path):
 def parse(path):
     """ncu --csv (metrics, one row per metric) -> {metric: value in base units}; or an .ncu-rep."""
     text = open(path).read()
-    if path.endswith(".ncu-rep") or '"Metric Name"' not in text.split("\n", 1)[0]:
+    hdr_line = next((l for l in text.split("\n") if l.startswith('"ID"')), "")   # ncu's banner lines may precede it
+    if path.endswith(".ncu-rep") or '"Metric Name"' not in hdr_line:
         return parse_rep(path)
     start = text.index('"ID"')
     rows = list(csv.DictReader(io.StringIO(text[start:])))
