@@ -117,6 +117,9 @@ struct WarpScratch {
 #ifndef CFUST_PF1_MASK
 #define CFUST_PF1_MASK ((1 << 3) | (1 << 4))
 #endif
+#ifndef CFUST_PFD_MASK
+#define CFUST_PFD_MASK 0   // the same one-point-ahead loads in sov_direct (SOV-direct estimator); see profiles/r02f_ab_direct.log
+#endif
 template <int Q>
 struct Tune {
     static constexpr bool XT = Q == CFUST_SOV_XT;
@@ -377,8 +380,30 @@ __device__ __noinline__ bool sov_direct(const double *b, const double *S, int ld
     for (int k = 0; k < Q; ++k) F3[k] = 0.0;
 #pragma unroll
     for (int k = 0; k < NT; ++k) F4[k] = 0.0;
+    // CFUST_PFD_MASK bit q: the chi node, lattice coordinates and log-V node of the next point are
+    // loaded one point ahead of the chain that consumes them (as sov_lane_sum's PF; same values in
+    // the same order, results bitwise unchanged).
+    constexpr bool PFD = (CFUST_PFD_MASK >> Q) & 1;
+    double sn1 = 0.0, lvn1 = 0.0, wn1[Q];
+    if constexpr (PFD) {
+        sn1 = __ldg(chi + lane);
+        if (!sn) lvn1 = __ldg(lv + lane);
+#pragma unroll
+        for (int k = 0; k < Q; ++k) wn1[k] = __ldg(W + (k + 1) * M + lane);
+    }
     for (int l = lane; l < M; l += 32) {
-        const double s = __ldg(chi + l);
+        double s, lvl = 0.0, wl[Q];
+        if constexpr (PFD) {
+            const int ln = (l + 32 < M) ? l + 32 : l;   // (the last point re-reads itself)
+            s = sn1;
+            sn1 = __ldg(chi + ln);
+            lvl = lvn1;
+            if (!sn) lvn1 = __ldg(lv + ln);
+#pragma unroll
+            for (int k = 0; k < Q; ++k) { wl[k] = wn1[k]; wn1[k] = __ldg(W + (k + 1) * M + ln); }
+        } else {
+            s = __ldg(chi + l);
+        }
         double e = Phi(s * binv[0]);
         double f = e;
         double xi[Q];
@@ -391,7 +416,7 @@ __device__ __noinline__ bool sov_direct(const double *b, const double *S, int ld
                 e = Phi(a);
                 f *= e;
             }
-            double u = __ldg(W + (k + 1) * M + l) * e;
+            double u = (PFD ? wl[k] : __ldg(W + (k + 1) * M + l)) * e;
             u = clamp_u(u, UMIN, UMAX);
             xi[k] = Phiinv(u);
         }
@@ -400,7 +425,7 @@ __device__ __noinline__ bool sov_direct(const double *b, const double *S, int ld
         const double fw = f * w;
         F += f;
         FW += fw;
-        if (!sn) FL = fma(f, __ldg(lv + l) - lrho, FL);
+        if (!sn) FL = fma(f, (PFD ? lvl : __ldg(lv + l)) - lrho, FL);
         double U[Q];
 #pragma unroll
         for (int k = 0; k < Q; ++k) {
