@@ -118,7 +118,7 @@ struct WarpScratch {
 #define CFUST_PF1_MASK ((1 << 3) | (1 << 4))
 #endif
 #ifndef CFUST_PFD_MASK
-#define CFUST_PFD_MASK 0   // the same one-point-ahead loads in sov_direct (SOV-direct estimator); see profiles/r02f_ab_direct.log
+#define CFUST_PFD_MASK 0x7e   // the same one-point-ahead loads in sov_direct (SOV-direct estimator), q = 1..6: cfg5 -8.8 %, cfg2 -2.5 %, cfg4 -2.3 %, cfg1 -1 % (profiles/r02g2_ab_direct.log)
 #endif
 template <int Q>
 struct Tune {

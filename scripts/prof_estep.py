@@ -26,7 +26,7 @@ if a.full_slice:
 else:
     cfg = synth.with_n(base, a.n)
     y, init, _ = synth.make_problem(cfg)
-em = cf.CfustEM(y, cfg.g, cfg.q, init, synth.lattice_inputs(cfg), timing=True,
+em = cf.CfustEM(y, cfg.g, cfg.q, init, synth.lattice_inputs(cfg, direct=a.estimator == "direct"), timing=True,
                 **({"estimator": "direct"} if a.estimator == "direct" else {}))
 for _ in range(a.em_iters):
     em.iterate()
